@@ -1,0 +1,211 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the UNMODIFIED reference library (compiled by
+// oracle/Makefile straight from /root/reference/proj/src into
+// oracle/_ref/librsfref*.so).  It lets tests/ and bench.py's reference arm
+// call the reference's own public C++ API (include/rsf/*.hpp) from ctypes:
+// rsf::evolve / init_evolution / evolve_step / energy / extract_mask, the
+// phantom generator, perturb and init_phi.  No reference source is copied
+// here; every call goes to the reference's compiled code.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "rsf/phantom.hpp"
+#include "rsf/rsf.hpp"
+#include "rsf/seeding.hpp"
+#include "rsf/validation.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+struct RefParams {  // field-for-field rsf::RsfParams (rsf.hpp:13-26)
+  double sigma1, sigma2, alpha, beta, epsilon, dt;
+  int32_t max_iters;
+  double convergence_fraction, denom_floor, grad_floor;
+};
+
+rsf::RsfParams to_ref(const RefParams* p) {
+  rsf::RsfParams r;
+  r.sigma1 = p->sigma1;
+  r.sigma2 = p->sigma2;
+  r.alpha = p->alpha;
+  r.beta = p->beta;
+  r.epsilon = p->epsilon;
+  r.dt = p->dt;
+  r.max_iters = p->max_iters;
+  r.convergence_fraction = p->convergence_fraction;
+  r.denom_floor = p->denom_floor;
+  r.grad_floor = p->grad_floor;
+  return r;
+}
+
+rsf::Volume make_vol(const float* d, int nx, int ny, int nz) {
+  rsf::Volume v(nx, ny, nz);
+  std::memcpy(v.data.data(), d, v.voxels() * sizeof(float));
+  return v;
+}
+
+// 0 ok, 1 param, 2 shape, 3 blowup, 7 other
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const rsf::param_error*>(&e)) return 1;
+  if (dynamic_cast<const rsf::shape_error*>(&e)) return 2;
+  if (dynamic_cast<const rsf::blowup_error*>(&e)) return 3;
+  return 7;
+}
+
+struct RefState {
+  rsf::EvolutionState st;
+  rsf::EvolveWorkspace ws;
+  rsf::Volume I;
+  rsf::RsfParams p;
+};
+}  // namespace
+
+#define GUARD(...)                  \
+  try {                             \
+    __VA_ARGS__;                    \
+    return 0;                       \
+  } catch (const std::exception& e) { \
+    g_err = e.what();               \
+    return code_of(e);              \
+  }
+
+extern "C" {
+
+const char* rsfref_last_error() { return g_err.c_str(); }
+void rsfref_set_workers(int n) { rsf::set_worker_count(n); }
+int rsfref_workers() { return rsf::detail::effective_workers(); }
+
+int rsfref_evolve(const float* I, float* phi, int nx, int ny, int nz, const RefParams* p) {
+  GUARD({
+    rsf::Volume out = rsf::evolve(make_vol(phi, nx, ny, nz), make_vol(I, nx, ny, nz), to_ref(p));
+    std::memcpy(phi, out.data.data(), out.voxels() * sizeof(float));
+  })
+}
+
+int rsfref_state_create(void** out, const float* phi0, const float* I, int nx, int ny, int nz,
+                        const RefParams* p) {
+  GUARD({
+    auto* s = new RefState;
+    try {
+      s->p = to_ref(p);
+      s->I = make_vol(I, nx, ny, nz);
+      s->st = rsf::init_evolution(make_vol(phi0, nx, ny, nz), s->I, s->p);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  })
+}
+
+int rsfref_state_step(void* h, double* frac) {
+  auto* s = static_cast<RefState*>(h);
+  GUARD({ *frac = rsf::evolve_step(s->st, s->I, s->p, s->ws); })
+}
+
+int rsfref_state_phi(void* h, float* out) {
+  auto* s = static_cast<RefState*>(h);
+  std::memcpy(out, s->st.phi.data.data(), s->st.phi.voxels() * sizeof(float));
+  return 0;
+}
+
+int rsfref_state_set_phi(void* h, const float* in) {
+  auto* s = static_cast<RefState*>(h);
+  std::memcpy(s->st.phi.data.data(), in, s->st.phi.voxels() * sizeof(float));
+  return 0;
+}
+
+int rsfref_state_energy(void* h, float* out) {
+  auto* s = static_cast<RefState*>(h);
+  GUARD({
+    rsf::Volume E = rsf::energy(s->st, s->I, s->p);
+    std::memcpy(out, E.data.data(), E.voxels() * sizeof(float));
+  })
+}
+
+int rsfref_state_static(void* h, float* KI, float* KI2, float* imin, float* imax) {
+  auto* s = static_cast<RefState*>(h);
+  std::memcpy(KI, s->st.KI.data.data(), s->st.KI.voxels() * sizeof(float));
+  std::memcpy(KI2, s->st.KI2.data.data(), s->st.KI2.voxels() * sizeof(float));
+  *imin = s->st.i_min;
+  *imax = s->st.i_max;
+  return 0;
+}
+
+void rsfref_state_destroy(void* h) { delete static_cast<RefState*>(h); }
+
+int rsfref_convolve(const float* v, int nx, int ny, int nz, double sigma, float* out) {
+  GUARD({
+    rsf::Volume o = rsf::convolve_separable(make_vol(v, nx, ny, nz), rsf::gaussian_kernel(sigma));
+    std::memcpy(out, o.data.data(), o.voxels() * sizeof(float));
+  })
+}
+
+int rsfref_gaussian_kernel(double sigma, double* w, int cap, int* radius) {
+  GUARD({
+    rsf::Kernel1D k = rsf::gaussian_kernel(sigma);
+    if (static_cast<int>(k.weights.size()) > cap) throw rsf::param_error("cap");
+    std::memcpy(w, k.weights.data(), k.weights.size() * sizeof(double));
+    *radius = k.radius;
+  })
+}
+
+int rsfref_extract_mask(const float* phi, int nx, int ny, int nz, float* mask) {
+  GUARD({
+    rsf::Volume m = rsf::extract_mask(make_vol(phi, nx, ny, nz));
+    std::memcpy(mask, m.data.data(), m.voxels() * sizeof(float));
+  })
+}
+
+// generate_network (phantom.cpp:55-184) + perturb (phantom.cpp:186-214).
+int rsfref_phantom(int nx, int ny, int nz, int n_branches, double rmin, double rmax, double tortuosity,
+                   float fg, float bg, uint64_t seed, int tree_connected, double axial_blur,
+                   double noise_sigma, int contrast_axis, double lo, double hi, uint64_t noise_seed,
+                   float* image, float* gt) {
+  GUARD({
+    rsf::PhantomSpec s;
+    s.dims = {nx, ny, nz};
+    s.n_branches = n_branches;
+    s.radius_min = rmin;
+    s.radius_max = rmax;
+    s.tortuosity = tortuosity;
+    s.foreground = fg;
+    s.background = bg;
+    s.rng_seed = seed;
+    s.tree_connected = tree_connected != 0;
+    s.axial_blur_sigma = axial_blur;
+    rsf::PhantomResult r = rsf::generate_network(s);
+    rsf::PerturbSpec ps;
+    ps.gaussian_sigma = noise_sigma;
+    ps.contrast_axis = static_cast<rsf::Axis>(contrast_axis);
+    ps.contrast_lo = lo;
+    ps.contrast_hi = hi;
+    rsf::Volume img = rsf::perturb(r.image, ps, noise_seed);
+    std::memcpy(image, img.data.data(), img.voxels() * sizeof(float));
+    std::memcpy(gt, r.gt_mask.data.data(), r.gt_mask.voxels() * sizeof(float));
+  })
+}
+
+// init_phi (seeding.cpp:221-235); returns the seed count through *n_seeds.
+int rsfref_init_phi(const float* vol, int nx, int ny, int nz, double sigma_b, double threshold, double nms,
+                    int dark, double seed_radius, float* phi, int* n_seeds) {
+  GUARD({
+    rsf::BlobParams bp;
+    bp.sigma_b = sigma_b;
+    bp.response_threshold = threshold;
+    bp.nms_radius = nms;
+    bp.polarity = dark ? rsf::Polarity::dark_on_bright : rsf::Polarity::bright_on_dark;
+    auto [p, seeds] = rsf::init_phi(make_vol(vol, nx, ny, nz), bp, seed_radius);
+    std::memcpy(phi, p.data.data(), p.voxels() * sizeof(float));
+    *n_seeds = static_cast<int>(seeds.points.size());
+  })
+}
+
+double rsfref_dice(const float* a, const float* b, int nx, int ny, int nz) {
+  return rsf::dice(make_vol(a, nx, ny, nz), make_vol(b, nx, ny, nz));
+}
+
+}  // extern "C"
