@@ -1,0 +1,204 @@
+/*
+ * rsfg.h -- C-ABI of the B200-native RSF level-set evolution library
+ * (librsfg.so).  This is the drop-in boundary for the reference hot path
+ * `rsf::evolve` / `init_evolution` / `evolve_step` / `energy` /
+ * `extract_mask` (reference: /root/reference/proj/include/rsf/rsf.hpp:13-101,
+ * src/rsf.cpp:293-396).  Plain pointers and sizes only; no C++ or torch types
+ * cross it.  A C++ wrapper with the reference's exact signatures and
+ * exception types lives in include/rsfgpu.hpp.
+ *
+ * Layout (same as rsf::Volume, volume.hpp:35-40): fp32, x fastest,
+ * index(x,y,z) = x + nx*(y + ny*z).  Inside the contour phi < 0.
+ *
+ * Errors: every int-returning call returns one of RSFG_* below;
+ * rsfg_last_error() gives the calling thread's message (same text as the
+ * reference exception where one exists).  All calls are thread-safe: a
+ * state/slab object must not be used from two threads at once, distinct
+ * objects may (each owns its CUDA stream, like rsf::evolve being reentrant,
+ * core.hpp:50-52).  Results are deterministic (bitwise) run to run and for
+ * any slab decomposition.
+ */
+#ifndef RSFG_H_
+#define RSFG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSFG_OK 0
+#define RSFG_ERR_PARAM 1  /* rsf::param_error  (rsf.cpp:10-20, ops.cpp:10-12)   */
+#define RSFG_ERR_SHAPE 2  /* rsf::shape_error  (volume.cpp:35-39, ops.cpp:201) */
+#define RSFG_ERR_BLOWUP 3 /* rsf::blowup_error (rsf.cpp:346-352)               */
+#define RSFG_ERR_CUDA 4
+#define RSFG_ERR_COMM 5
+#define RSFG_ERR_OOM 6
+#define RSFG_ERR_STATE 7 /* misuse: null handle, invalidated state, ...        */
+
+/* Field-for-field rsf::RsfParams (rsf.hpp:13-26); defaults via
+ * rsfg_params_default().  north_star names: sigma -> sigma1 (+sigma2),
+ * nu -> alpha, lambda1 = lambda2 -> beta, mu -> 1 (fixed), eps -> epsilon,
+ * dt -> dt, iterations -> max_iters. */
+typedef struct rsfg_params {
+  double sigma1;
+  double sigma2;
+  double alpha;
+  double beta;
+  double epsilon;
+  double dt;
+  int32_t max_iters;
+  double convergence_fraction;
+  double denom_floor;
+  double grad_floor;
+} rsfg_params;
+
+/* Region-average convolution form:
+ *   RSFG_FIELDS_4: convolve H-, H-*I, H+, H+*I like the reference (rsf.cpp:183-194);
+ *   RSFG_FIELDS_2: convolve H-, H-*I only; K*H+ = 1 - K*H-, K*(H+ I) = K1*I - K*(H- I)
+ *                  (exact algebra, fp32 rounding differs; half the convolution work). */
+#define RSFG_FIELDS_4 4
+#define RSFG_FIELDS_2 2
+
+typedef struct rsfg_options {
+  int32_t device;      /* CUDA device ordinal (default 0)                               */
+  int32_t fields;      /* RSFG_FIELDS_2 or RSFG_FIELDS_4 (default: RSFG_FIELDS_2)      */
+  int32_t check_every; /* evolve/run: host checks blowup every N steps (default 25)     */
+  int32_t use_graphs;  /* capture per-step launches in CUDA graphs (default 1)          */
+  int32_t reserved[4];
+} rsfg_options;
+
+typedef struct rsfg_report {
+  int32_t iterations;             /* steps completed                                  */
+  int32_t blowup_iteration;       /* 1-based iteration of the first non-finite phi, 0 */
+  int32_t blowup_x, blowup_y, blowup_z;
+  double last_sign_change_fraction;
+  double ms_h2d, ms_init, ms_loop, ms_d2h; /* CUDA-event timings of the call's phases    */
+  int64_t gpu_launches;           /* kernels launched by the call                     */
+} rsfg_report;
+
+/* Called every stop_every iterations with the current phi (host copy);
+ * return nonzero to stop (rsf::StopCheck, rsf.hpp:89, rsf.cpp:379-381). */
+typedef int (*rsfg_stop_fn)(const float* phi, int32_t nx, int32_t ny, int32_t nz, int32_t iteration,
+                            void* user);
+
+const char* rsfg_last_error(void);
+const char* rsfg_version(void);
+void rsfg_params_default(rsfg_params* p);
+void rsfg_options_default(rsfg_options* o);
+/* RsfParams::validate (rsf.cpp:10-20). */
+int rsfg_params_validate(const rsfg_params* p);
+/* gaussian_kernel (ops.cpp:9-29): radius = ceil(3 sigma), f64 weights. */
+int rsfg_gaussian_kernel(double sigma, double* weights, int32_t cap, int32_t* radius);
+
+/* rsf::evolve (rsf.hpp:97-98, rsf.cpp:359-384) on HOST buffers: phi_inout holds
+ * phi0 on entry and the evolved phi on return.  nz == 1 is evolved as a
+ * duplicated slice pair (rsf.cpp:363-372).  stop may be NULL.  report may be
+ * NULL. */
+int rsfg_evolve(const float* image, float* phi_inout, int32_t nx, int32_t ny, int32_t nz,
+                const rsfg_params* p, const rsfg_options* o, rsfg_stop_fn stop, void* user,
+                int32_t stop_every, rsfg_report* report);
+
+/* rsf::extract_mask (rsf.cpp:386-396): mask = phi < 0 ? 1 : 0, on the GPU. */
+int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device);
+
+/* ---- stateful stepping: rsf::init_evolution / evolve_step / energy ------- */
+typedef struct rsfg_state rsfg_state;
+
+/* init_evolution (rsf.cpp:293-313): uploads phi0 and I, computes the static
+ * convolutions and [min I, max I].  Ownership: the state owns its device
+ * buffers; host buffers are only read during the call. */
+int rsfg_state_create(rsfg_state** out, const float* phi0, const float* image, int32_t nx, int32_t ny,
+                      int32_t nz, const rsfg_params* p, const rsfg_options* o);
+/* Same, from DEVICE pointers on the state's device (no host round trip). */
+int rsfg_state_create_device(rsfg_state** out, const float* d_phi0, const float* d_image, int32_t nx,
+                             int32_t ny, int32_t nz, const rsfg_params* p, const rsfg_options* o);
+/* evolve_step (rsf.cpp:324-357): one explicit step; returns the sign-change
+ * fraction.  On blowup returns RSFG_ERR_BLOWUP and leaves phi unchanged. */
+int rsfg_state_step(rsfg_state* s, double* sign_change_fraction);
+/* n steps with no per-step host synchronisation (blowup checked every
+ * check_every steps; on blowup the state is invalidated). */
+int rsfg_state_run(rsfg_state* s, int32_t n, rsfg_report* report);
+int rsfg_state_energy(rsfg_state* s, float* E_host); /* energy() (rsf.cpp:315-322) */
+/* KernelProfile analogue (rsf.hpp:64-69, profiling.cpp:8-47): runs `steps`
+ * steps and writes the mean CUDA-event milliseconds of each kernel group to
+ * ms[0..RSFG_PROFILE_COUNT); names from rsfg_profile_name(i). */
+#define RSFG_PROFILE_COUNT 2
+int rsfg_state_profile(rsfg_state* s, int32_t steps, double* ms);
+const char* rsfg_profile_name(int32_t i);
+int rsfg_state_read_phi(rsfg_state* s, float* phi_host);
+int rsfg_state_write_phi(rsfg_state* s, const float* phi_host);
+int rsfg_state_mask(rsfg_state* s, float* mask_host);
+int rsfg_state_iteration(const rsfg_state* s, int32_t* iteration);
+/* Device pointer of the current phi (valid until the next step). */
+int rsfg_state_device_phi(rsfg_state* s, float** d_phi);
+/* The CUDA stream (cudaStream_t) the state launches on. */
+int rsfg_state_stream(rsfg_state* s, void** stream);
+int rsfg_state_sync(rsfg_state* s);
+/* Kernels launched by this state so far. */
+int64_t rsfg_state_launches(const rsfg_state* s);
+void rsfg_state_destroy(rsfg_state* s);
+
+/* ---- z-slab SPMD primitives (multi-GPU) -------------------
+ * A slab owns global planes [z0, z1) of an nx*ny*nz volume and holds
+ * [zb, ze) = [max(z0-h,0), min(z1+h,nz)), h = max(R1, R2, 2).  Per step the
+ * caller exchanges the h phi planes on each interior face (send/recv views
+ * from rsfg_slab_halo) with its z-neighbours -- NCCL send/recv, P2P, or a
+ * plain device copy -- between step_interior and step_finish, which both run
+ * on the slab's stream (or the one set by rsfg_slab_set_stream).  Results
+ * are bitwise identical to the monolithic volume. */
+typedef struct rsfg_slab rsfg_slab;
+
+int rsfg_slab_create(rsfg_slab** out, int32_t nx, int32_t ny, int32_t nz, int32_t z0, int32_t z1,
+                     const rsfg_params* p, const rsfg_options* o);
+int rsfg_slab_geometry(const rsfg_slab* s, int32_t* zb, int32_t* ze, int32_t* halo);
+/* Host planes [zb, ze) of phi0 and I. */
+int rsfg_slab_upload(rsfg_slab* s, const float* phi_held, const float* image_held);
+/* min/max of I over the owned planes; the caller reduces across slabs and
+ * passes the global pair to rsfg_slab_init (volume.cpp:25-33 semantics). */
+int rsfg_slab_local_range(rsfg_slab* s, float* i_min, float* i_max);
+int rsfg_slab_init(rsfg_slab* s, float i_min, float i_max);
+/* side 0 = toward z=0, 1 = toward z=nz-1.  Device pointers into the CURRENT
+ * phi buffer: *send = h owned planes next to that face, *recv = the h halo
+ * planes beyond it; *bytes = 0 on a global face. */
+int rsfg_slab_halo(rsfg_slab* s, int32_t side, void** send, void** recv, int64_t* bytes);
+int rsfg_slab_set_stream(rsfg_slab* s, void* stream);
+/* Single-process halo exchange between z-adjacent slabs `lo` (owns planes
+ * below) and `hi`, on the same or different devices (peer copies over
+ * NVLink): stream-ordered after both slabs' previous step, before their next
+ * step_finish.  The in-process backend of the decomposition (tests, P2P). */
+int rsfg_slab_exchange(rsfg_slab* lo, rsfg_slab* hi);
+int rsfg_slab_step_interior(rsfg_slab* s); /* work that needs no halo */
+int rsfg_slab_step_finish(rsfg_slab* s);   /* the rest; swaps phi      */
+/* Sign changes / first non-finite global index (-1) of the last step (syncs). */
+int rsfg_slab_counters(rsfg_slab* s, int64_t* sign_changes, int64_t* first_bad);
+int rsfg_slab_download(rsfg_slab* s, float* phi_owned);
+int rsfg_slab_device_phi(rsfg_slab* s, float** d_phi_held);
+int64_t rsfg_slab_launches(const rsfg_slab* s);
+void rsfg_slab_destroy(rsfg_slab* s);
+
+/* ---- synthetic inputs (reference phantom.cpp:55-214) ------ */
+typedef struct rsfg_phantom_spec {
+  int32_t nx, ny, nz;
+  int32_t n_branches;
+  double radius_min, radius_max, tortuosity;
+  float foreground, background;
+  uint64_t rng_seed;
+  int32_t tree_connected;
+  double axial_blur_sigma;
+  /* perturb (phantom.cpp:186-214) */
+  double noise_sigma;
+  int32_t contrast_axis; /* 0 none, 1 x, 2 y, 3 z */
+  double contrast_lo, contrast_hi;
+  uint64_t noise_seed;
+} rsfg_phantom_spec;
+
+void rsfg_phantom_default(rsfg_phantom_spec* s);
+/* Tube-network image (perturbed) and ground-truth mask, host buffers. */
+int rsfg_phantom(const rsfg_phantom_spec* s, float* image, float* gt_mask);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSFG_H_ */

@@ -1,0 +1,23 @@
+"""B200-native RSF level-set evolution (arXiv 2404.02813 hot path).
+
+The product is librsfg.so (CUDA sm_100a kernels behind the C-ABI in
+include/rsfg.h).  This package is the Python mirror of the reference API
+for tests and benchmarks; see api.py.
+"""
+from .api import (  # noqa: F401
+    BlowupError,
+    EvolutionState,
+    ParamError,
+    RsfParams,
+    ShapeError,
+    dice,
+    energy,
+    evolve,
+    evolve_step,
+    extract_mask,
+    gaussian_kernel,
+    init_evolution,
+    phantom,
+    threshold_phi0,
+)
+from ._lib import LIB_PATH, load  # noqa: F401

@@ -1,0 +1,282 @@
+"""Python mirror of the reference RSF API over the CUDA C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/rsf/rsf.hpp:13-101):
+
+    RsfParams, evolve(phi0, I, p, stop=None, stop_every=25),
+    init_evolution(phi0, I, p) -> EvolutionState, evolve_step(state),
+    energy(state), extract_mask(phi)
+
+with exceptions ParamError / ShapeError / BlowupError standing in for
+rsf::param_error / shape_error / blowup_error.  Volumes are numpy float32
+arrays shaped (nz, ny, nx) -- the reference's x-fastest layout
+(volume.hpp:35-40).  Everything runs in librsfg.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, fields as dc_fields
+
+import numpy as np
+
+from . import _lib as L
+
+
+class RsfError(RuntimeError):
+    pass
+
+
+class ParamError(RsfError, ValueError):
+    """rsf::param_error (core.hpp:11-14)."""
+
+
+class ShapeError(RsfError, ValueError):
+    """rsf::shape_error (core.hpp:16-20)."""
+
+
+class BlowupError(RsfError):
+    """rsf::blowup_error (core.hpp:28-32)."""
+
+
+class CudaError(RsfError):
+    pass
+
+
+_ERRORS = {L.RSFG_ERR_PARAM: ParamError, L.RSFG_ERR_SHAPE: ShapeError, L.RSFG_ERR_BLOWUP: BlowupError}
+
+
+def check(rc: int) -> None:
+    if rc != L.RSFG_OK:
+        raise _ERRORS.get(rc, CudaError)(f"[rsfg {rc}] {L.last_error()}")
+
+
+@dataclass
+class RsfParams:
+    """rsf::RsfParams (rsf.hpp:13-26), same defaults."""
+
+    sigma1: float = 5.0
+    sigma2: float = 0.0
+    alpha: float = 58.5225
+    beta: float = 0.1
+    epsilon: float = 1.0
+    dt: float = 0.06
+    max_iters: int = 100
+    convergence_fraction: float = 0.0
+    denom_floor: float = 1e-8
+    grad_floor: float = 1e-8
+
+    def to_c(self) -> L.rsfg_params:
+        return L.rsfg_params(**{f.name: getattr(self, f.name) for f in dc_fields(self)})
+
+    def validate(self) -> None:
+        p = self.to_c()
+        check(L.load().rsfg_params_validate(C.byref(p)))
+
+
+def options(fields: int = 2, device: int = 0, check_every: int = 25) -> L.rsfg_options:
+    o = L.rsfg_options()
+    L.load().rsfg_options_default(C.byref(o))
+    o.fields, o.device, o.check_every = fields, device, check_every
+    return o
+
+
+def _vol(a, name="volume") -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.ndim == 2:
+        a = a[None]
+    if a.ndim != 3:
+        raise ShapeError(f"{name}: expected (nz, ny, nx) array, got shape {a.shape}")
+    return a
+
+
+def _check_same(a, b, what):
+    if a.shape != b.shape:
+        sa = "x".join(map(str, a.shape[::-1]))
+        sb = "x".join(map(str, b.shape[::-1]))
+        raise ShapeError(f"{what}: dims mismatch {sa} vs {sb}")  # volume.cpp:35-39
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def gaussian_kernel(sigma: float) -> np.ndarray:
+    """gaussian_kernel (ops.cpp:9-29)."""
+    w = (C.c_double * 1024)()
+    r = C.c_int32()
+    check(L.load().rsfg_gaussian_kernel(sigma, w, 1024, C.byref(r)))
+    return np.array(w[: 2 * r.value + 1])
+
+
+def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, *, fields: int = 2, device: int = 0,
+           report: L.rsfg_report | None = None) -> np.ndarray:
+    """rsf::evolve (rsf.cpp:359-384): returns the evolved phi (same shape as phi0)."""
+    squeeze = np.ndim(phi0) == 2
+    phi = _vol(phi0, "phi0").copy()
+    img = _vol(I, "I")
+    _check_same(phi, img, "evolve")
+    nz, ny, nx = phi.shape
+    cp = p.to_c()
+    opt = options(fields, device)
+    rep = report if report is not None else L.rsfg_report()
+    cb = L.STOP_FN(0)
+    if stop is not None:
+        def _cb(ptr, cx, cy, cz, it, _u):
+            arr = np.ctypeslib.as_array(ptr, shape=(cz, cy, cx)).copy()
+            return 1 if stop(arr, it) else 0
+        cb = L.STOP_FN(_cb)
+    check(L.load().rsfg_evolve(_ptr(img), _ptr(phi), nx, ny, nz, C.byref(cp), C.byref(opt), cb, None,
+                               stop_every, C.byref(rep)))
+    return phi[0] if squeeze else phi
+
+
+def extract_mask(phi, device: int = 0) -> np.ndarray:
+    """rsf::extract_mask (rsf.cpp:386-396): 1 where phi < 0."""
+    a = np.ascontiguousarray(phi, dtype=np.float32)
+    out = np.empty_like(a)
+    check(L.load().rsfg_extract_mask(_ptr(a), _ptr(out), a.size, device))
+    return out
+
+
+class EvolutionState:
+    """rsf::EvolutionState (rsf.hpp:54-61) held on the GPU."""
+
+    def __init__(self, phi0, I, p: RsfParams, *, fields: int = 2, device: int = 0, check_every: int = 25):
+        phi = _vol(phi0, "phi0")
+        img = _vol(I, "I")
+        _check_same(phi, img, "init_evolution")
+        self.shape = phi.shape
+        self.p = p
+        self._h = C.c_void_p()
+        cp = p.to_c()
+        opt = options(fields, device, check_every)
+        nz, ny, nx = phi.shape
+        check(L.load().rsfg_state_create(C.byref(self._h), _ptr(phi), _ptr(img), nx, ny, nz, C.byref(cp),
+                                         C.byref(opt)))
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    @property
+    def iteration(self) -> int:
+        it = C.c_int32()
+        check(L.load().rsfg_state_iteration(self._h, C.byref(it)))
+        return it.value
+
+    @property
+    def phi(self) -> np.ndarray:
+        out = np.empty(self.shape, np.float32)
+        check(L.load().rsfg_state_read_phi(self._h, _ptr(out)))
+        return out
+
+    @phi.setter
+    def phi(self, value) -> None:
+        a = _vol(value, "phi")
+        _check_same(a, np.empty(self.shape, np.float32), "phi")
+        check(L.load().rsfg_state_write_phi(self._h, _ptr(a)))
+
+    def step(self) -> float:
+        f = C.c_double()
+        check(L.load().rsfg_state_step(self._h, C.byref(f)))
+        return f.value
+
+    def run(self, n: int) -> L.rsfg_report:
+        rep = L.rsfg_report()
+        check(L.load().rsfg_state_run(self._h, n, C.byref(rep)))
+        return rep
+
+    def profile(self, steps: int) -> dict:
+        """Mean CUDA-event ms per kernel group over `steps` steps (KernelProfile analogue)."""
+        ms = (C.c_double * 2)()
+        lib = L.load()
+        check(lib.rsfg_state_profile(self._h, steps, ms))
+        return {lib.rsfg_profile_name(i).decode().split(":")[0]: ms[i] for i in range(2)}
+
+    def energy(self) -> np.ndarray:
+        out = np.empty(self.shape, np.float32)
+        check(L.load().rsfg_state_energy(self._h, _ptr(out)))
+        return out
+
+    def mask(self) -> np.ndarray:
+        out = np.empty(self.shape, np.float32)
+        check(L.load().rsfg_state_mask(self._h, _ptr(out)))
+        return out
+
+    def device_phi(self) -> int:
+        d = C.c_void_p()
+        check(L.load().rsfg_state_device_phi(self._h, C.byref(d)))
+        return d.value
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(L.load().rsfg_state_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def sync(self) -> None:
+        check(L.load().rsfg_state_sync(self._h))
+
+    def launches(self) -> int:
+        return int(L.load().rsfg_state_launches(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            L.load().rsfg_state_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def init_evolution(phi0, I, p: RsfParams, **kw) -> EvolutionState:
+    """rsf::init_evolution (rsf.cpp:293-313)."""
+    p.validate()
+    return EvolutionState(phi0, I, p, **kw)
+
+
+def evolve_step(state: EvolutionState) -> float:
+    """rsf::evolve_step (rsf.cpp:324-357): returns the sign-change fraction."""
+    return state.step()
+
+
+def energy(state: EvolutionState) -> np.ndarray:
+    """rsf::energy (rsf.cpp:315-322)."""
+    return state.energy()
+
+
+def phantom(nx, ny, nz, n_branches=12, radius_min=2.0, radius_max=4.0, tortuosity=0.25, foreground=200.0,
+            background=50.0, rng_seed=1, tree_connected=True, axial_blur_sigma=0.0, noise_sigma=20.0,
+            contrast_axis=0, contrast_lo=1.0, contrast_hi=1.0, noise_seed=7):
+    """Tube-network phantom + perturb (reference phantom.cpp:55-214); returns (image, gt_mask)."""
+    s = L.rsfg_phantom_spec()
+    L.load().rsfg_phantom_default(C.byref(s))
+    for k, v in dict(nx=nx, ny=ny, nz=nz, n_branches=n_branches, radius_min=radius_min, radius_max=radius_max,
+                     tortuosity=tortuosity, foreground=foreground, background=background, rng_seed=rng_seed,
+                     tree_connected=int(tree_connected), axial_blur_sigma=axial_blur_sigma,
+                     noise_sigma=noise_sigma, contrast_axis=contrast_axis, contrast_lo=contrast_lo,
+                     contrast_hi=contrast_hi, noise_seed=noise_seed).items():
+        setattr(s, k, v)
+    img = np.empty((nz, ny, nx), np.float32)
+    gt = np.empty((nz, ny, nx), np.float32)
+    rc = L.load().rsfg_phantom(C.byref(s), _ptr(img), _ptr(gt))
+    if rc != 0:
+        raise ParamError(f"phantom spec rejected (rc={rc})")
+    return img, gt
+
+
+def threshold_phi0(image, level: float = 125.0, inside: float = -2.0, outside: float = 2.0) -> np.ndarray:
+    """Documented threshold initialisation for throughput runs (SURVEY.md 8(d) cfg 4)."""
+    return np.where(np.asarray(image) > level, np.float32(inside), np.float32(outside)).astype(np.float32)
+
+
+def dice(a, b) -> float:
+    """rsf::dice (validation.cpp:41-45) on masks (> 0.5 is foreground)."""
+    a = np.asarray(a) > 0.5
+    b = np.asarray(b) > 0.5
+    na, nb = int(a.sum()), int(b.sum())
+    if na + nb == 0:
+        return 1.0
+    return 2.0 * int(np.logical_and(a, b).sum()) / (na + nb)

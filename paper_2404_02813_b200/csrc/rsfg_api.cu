@@ -1,0 +1,904 @@
+// rsfg_api.cu -- the C-ABI (include/rsfg.h): contexts, buffers, the step
+// schedule, error mapping.  Host code; kernels live in rsfg_kernels.cu.
+//
+// One engine type serves both the monolithic state (rsf::init_evolution /
+// evolve_step, rsf.cpp:293-357) and z-slabs: a state is the
+// slab [0, nz) with no halo.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rsfg.h"
+#include "rsfg_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      const int code_ = (e_ == cudaErrorMemoryAllocation) ? RSFG_ERR_OOM : RSFG_ERR_CUDA;   \
+      return fail(code_, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #expr); \
+    }                                                                                       \
+  } while (0)
+
+// rsf::RsfParams::validate (rsf.cpp:10-20), same messages.
+int validate(const rsfg_params* p) {
+  if (!p) return fail(RSFG_ERR_PARAM, "RsfParams: null");
+  if (p->sigma1 < 0.0) return fail(RSFG_ERR_PARAM, "RsfParams: sigma1 must be >= 0");
+  if (p->sigma2 < 0.0) return fail(RSFG_ERR_PARAM, "RsfParams: sigma2 must be >= 0");
+  if (!(p->epsilon > 0.0)) return fail(RSFG_ERR_PARAM, "RsfParams: epsilon must be > 0");
+  if (!(p->dt > 0.0)) return fail(RSFG_ERR_PARAM, "RsfParams: dt must be > 0");
+  if (p->max_iters < 1) return fail(RSFG_ERR_PARAM, "RsfParams: max_iters must be >= 1");
+  if (p->convergence_fraction < 0.0 || p->convergence_fraction >= 1.0)
+    return fail(RSFG_ERR_PARAM, "RsfParams: convergence_fraction must be in [0,1)");
+  if (!(p->denom_floor > 0.0)) return fail(RSFG_ERR_PARAM, "RsfParams: denom_floor must be > 0");
+  if (!(p->grad_floor > 0.0)) return fail(RSFG_ERR_PARAM, "RsfParams: grad_floor must be > 0");
+  return RSFG_OK;
+}
+
+// gaussian_kernel (ops.cpp:9-29): f64 weights exp(-i^2/(2 sigma^2)) / sum.
+int gaussian(double sigma, std::vector<double>& w) {
+  if (sigma < 0.0 || !std::isfinite(sigma)) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "gaussian_kernel: sigma must be >= 0, got %f", sigma);
+    return fail(RSFG_ERR_PARAM, buf);
+  }
+  if (sigma == 0.0) {
+    w.assign(1, 1.0);
+    return RSFG_OK;
+  }
+  const int r = (int)std::ceil(3.0 * sigma);
+  w.assign(2 * r + 1, 0.0);
+  double sum = 0.0;
+  for (int i = -r; i <= r; ++i) {
+    const double v = std::exp(-((double)i * i) / (2.0 * sigma * sigma));
+    w[i + r] = v;
+    sum += v;
+  }
+  for (double& v : w) v /= sum;
+  return RSFG_OK;
+}
+
+int make_taps(double sigma, rsfg::Taps& t) {
+  std::vector<double> w;
+  if (int rc = gaussian(sigma, w)) return rc;
+  if ((int)w.size() > rsfg::kMaxTaps - 1)
+    return fail(RSFG_ERR_PARAM, "sigma too large for this build (radius > 31)");
+  std::memset(&t, 0, sizeof t);
+  t.r = (int)(w.size() / 2);
+  for (size_t i = 0; i < w.size(); ++i) t.w[i] = (float)w[i];
+  return RSFG_OK;
+}
+
+constexpr int kSlots = 64;  // per-iteration counter ring
+
+}  // namespace
+
+// ------------------------------------------------------------------ engine
+struct rsfg_slab {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nx = 0, ny = 0, nz = 0, z0 = 0, z1 = 0, zb = 0, ze = 0, h = 0;
+  rsfg_params p{};
+  int fields = 2, check_every = 25;
+  rsfg::Taps t1{}, t2{}, tid{};
+  rsfg::StepConsts c{};
+  bool fast = true;
+  float* phi[2] = {nullptr, nullptr};
+  int cur = 0;
+  float* image = nullptr;
+  float* k1i = nullptr;
+  float* ki = nullptr;  // == image when sigma2 == 0
+  float2* P[2] = {nullptr, nullptr};
+  float2* scratch = nullptr;
+  unsigned long long* counters = nullptr;   // device [kSlots][2]
+  unsigned long long* h_counters = nullptr; // pinned mirror
+  unsigned int* mm = nullptr;               // device min/max scratch
+  int slot = 0;
+  int iteration = 0;
+  long long launches = 0;
+  bool valid = true;
+  bool initialized = false;
+
+  rsfg::Geom geom() const {
+    rsfg::Geom g;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    g.zb = zb;
+    g.ze = ze;
+    g.plane = (long long)nx * ny;
+    return g;
+  }
+  size_t held() const { return (size_t)(ze - zb) * (size_t)nx * ny; }
+  size_t owned() const { return (size_t)(z1 - z0) * (size_t)nx * ny; }
+  size_t off(int z) const { return (size_t)(z - zb) * (size_t)nx * ny; }
+};
+
+struct rsfg_state {
+  rsfg_slab e;
+};
+
+namespace {
+
+void release(rsfg_slab* s) {
+  if (!s) return;
+  cudaSetDevice(s->dev);
+  cudaFree(s->phi[0]);
+  cudaFree(s->phi[1]);
+  cudaFree(s->image);
+  cudaFree(s->k1i);
+  if (s->ki != s->image) cudaFree(s->ki);
+  cudaFree(s->P[0]);
+  cudaFree(s->P[1]);
+  cudaFree(s->scratch);
+  cudaFree(s->counters);
+  cudaFree(s->mm);
+  if (s->h_counters) cudaFreeHost(s->h_counters);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_params* p,
+          const rsfg_options* o) {
+  if (int rc = validate(p)) return rc;
+  rsfg_options opt;
+  rsfg_options_default(&opt);
+  if (o) opt = *o;
+  if (opt.fields != 2 && opt.fields != 4) return fail(RSFG_ERR_PARAM, "options.fields must be 2 or 4");
+  if (nx <= 0 || ny <= 0 || nz <= 0)
+    return fail(RSFG_ERR_SHAPE, "volume dims must be positive");
+  if (z0 < 0 || z1 > nz || z0 >= z1) return fail(RSFG_ERR_SHAPE, "slab range must satisfy 0 <= z0 < z1 <= nz");
+  s->p = *p;
+  s->fields = opt.fields;
+  s->check_every = std::min(std::max(opt.check_every, 1), kSlots);
+  s->dev = opt.device;
+  if (int rc = make_taps(p->sigma1, s->t1)) return rc;
+  if (int rc = make_taps(p->sigma2, s->t2)) return rc;
+  std::memset(&s->tid, 0, sizeof s->tid);
+  s->tid.w[0] = 1.0f;
+  s->tid.r = 0;
+  s->fast = rsfg::has_fast_radius(s->t1.r);
+  s->nx = nx;
+  s->ny = ny;
+  s->nz = nz;
+  s->z0 = z0;
+  s->z1 = z1;
+  s->h = std::max(std::max(s->t1.r, s->t2.r), 2);
+  s->zb = std::max(z0 - s->h, 0);
+  s->ze = std::min(z1 + s->h, nz);
+  // Halo planes come from the adjacent slab only: a slab with an interior
+  // face must be at least h planes thick (then every face exchanges h).
+  if ((z0 > 0 || z1 < nz) && z1 - z0 < s->h)
+    return fail(RSFG_ERR_SHAPE, "slab thinner than its halo (" + std::to_string(z1 - z0) + " < " +
+                                    std::to_string(s->h) + " planes)");
+  // Step scalars (rsf.cpp:86,105,118,142,161,334).
+  const double eps = p->epsilon;
+  s->c.inv_eps = (float)(1.0 / eps);
+  s->c.c_delta = (float)((1.0 / M_PI) * eps);
+  s->c.eps2 = (float)(eps * eps);
+  s->c.alpha = (float)p->alpha;
+  s->c.beta = (float)p->beta;
+  s->c.denom_floor = (float)p->denom_floor;
+  s->c.grad_floor = (float)p->grad_floor;
+  s->c.dt = p->dt;
+
+  CUDA_TRY(cudaSetDevice(s->dev));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->own_stream = true;
+  const size_t held = s->held();
+  CUDA_TRY(cudaMalloc(&s->phi[0], held * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&s->phi[1], held * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&s->image, held * sizeof(float)));
+  if (s->fields == 2) CUDA_TRY(cudaMalloc(&s->k1i, held * sizeof(float)));
+  if (s->t2.r > 0)
+    CUDA_TRY(cudaMalloc(&s->ki, held * sizeof(float)));
+  else
+    s->ki = s->image;
+  CUDA_TRY(cudaMalloc(&s->P[0], held * sizeof(float2)));
+  if (s->fields == 4) CUDA_TRY(cudaMalloc(&s->P[1], held * sizeof(float2)));
+  if (!s->fast) CUDA_TRY(cudaMalloc(&s->scratch, held * sizeof(float2) * (s->fields == 4 ? 4 : 2)));
+  CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
+  CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
+  // Never-read halo planes must still be finite memory: zero everything once.
+  CUDA_TRY(cudaMemsetAsync(s->phi[0], 0, held * sizeof(float), s->stream));
+  CUDA_TRY(cudaMemsetAsync(s->phi[1], 0, held * sizeof(float), s->stream));
+  return RSFG_OK;
+}
+
+int upload(rsfg_slab* s, const float* phi, const float* image, cudaMemcpyKind kind) {
+  CUDA_TRY(cudaSetDevice(s->dev));
+  const size_t bytes = s->held() * sizeof(float);
+  CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, bytes, kind, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(s->image, image, bytes, kind, s->stream));
+  return RSFG_OK;
+}
+
+int local_range(rsfg_slab* s, float* lo, float* hi) {
+  CUDA_TRY(cudaSetDevice(s->dev));
+  const unsigned int init[2] = {0xffffffffu, 0u};
+  CUDA_TRY(cudaMemcpyAsync(s->mm, init, sizeof init, cudaMemcpyHostToDevice, s->stream));
+  s->launches += rsfg::launch_minmax(s->geom(), s->image, s->z0, s->z1, s->mm, s->stream);
+  unsigned int out[2];
+  CUDA_TRY(cudaMemcpyAsync(out, s->mm, sizeof out, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  *lo = rsfg::decode_ordered(out[0]);
+  *hi = rsfg::decode_ordered(out[1]);
+  return RSFG_OK;
+}
+
+// init_evolution's static part (rsf.cpp:299-311): K1*I (fields=2) and
+// K2*I (sigma2 > 0) on the owned planes.  K2*I^2 is never formed: only
+// F- - F+ enters E and it cancels.
+int init_static(rsfg_slab* s, float i_min, float i_max) {
+  CUDA_TRY(cudaSetDevice(s->dev));
+  s->c.i_min = i_min;
+  s->c.i_max = i_max;
+  const rsfg::Geom g = s->geom();
+  float* tmp0 = reinterpret_cast<float*>(s->P[0]);
+  float* tmp1 = tmp0 + s->held();
+  if (s->fields == 2) {
+    if (s->t1.r > 0)
+      s->launches += rsfg::launch_convolve(g, s->t1, s->image, s->k1i, tmp0, tmp1, s->z0, s->z1, s->stream);
+    else
+      CUDA_TRY(cudaMemcpyAsync(s->k1i + s->off(s->z0), s->image + s->off(s->z0), s->owned() * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s->stream));
+  }
+  if (s->t2.r > 0)
+    s->launches += rsfg::launch_convolve(g, s->t2, s->image, s->ki, tmp0, tmp1, s->z0, s->z1, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  s->initialized = true;
+  return RSFG_OK;
+}
+
+int check_shape(const rsfg_slab* s) {
+  if (s->nx < 2 || s->ny < 2 || s->nz < 2) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "gradient: every axis needs extent >= 2, got %dx%dx%d", s->nx, s->ny, s->nz);
+    return fail(RSFG_ERR_SHAPE, buf);
+  }
+  return RSFG_OK;
+}
+
+rsfg::StepBuffers buffers(rsfg_slab* s, float* out) {
+  rsfg::StepBuffers b;
+  b.phi = s->phi[s->cur];
+  b.image = s->image;
+  b.k1i = s->k1i;
+  b.ki = s->ki;
+  b.P[0] = s->P[0];
+  b.P[1] = s->P[1];
+  b.out = out;
+  b.counters = s->counters + 2 * s->slot;
+  return b;
+}
+
+// xy work for planes [a, b) of the current phi.
+int xy_planes(rsfg_slab* s, int a, int b) {
+  if (b <= a) return RSFG_OK;
+  const rsfg::Geom g = s->geom();
+  int n;
+  if (s->fast) {
+    n = rsfg::launch_xy(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P[0], s->P[1], a, b,
+                        s->stream);
+  } else {
+    n = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
+                                  s->scratch, a, b, 0, 0, s->stream);
+  }
+  if (n < 0) return fail(RSFG_ERR_CUDA, "xy launch failed");
+  s->launches += n;
+  CUDA_TRY(cudaGetLastError());
+  return RSFG_OK;
+}
+
+int step_interior(rsfg_slab* s) {
+  if (!s->valid) return fail(RSFG_ERR_STATE, "state invalidated by an earlier blowup or error");
+  if (!s->initialized) return fail(RSFG_ERR_STATE, "slab not initialised");
+  if (int rc = check_shape(s)) return rc;
+  CUDA_TRY(cudaSetDevice(s->dev));
+  return xy_planes(s, s->z0, s->z1);
+}
+
+// Halo xy work, then kernel 2 over the owned planes; mode kUpdate swaps.
+int step_finish(rsfg_slab* s, rsfg::StepMode mode, float* out) {
+  CUDA_TRY(cudaSetDevice(s->dev));
+  const int r = s->t1.r;
+  if (int rc = xy_planes(s, std::max(s->z0 - r, s->zb), s->z0)) return rc;
+  if (int rc = xy_planes(s, s->z1, std::min(s->z1 + r, s->ze))) return rc;
+  const rsfg::Geom g = s->geom();
+  if (mode == rsfg::kUpdate) {
+    // slot: [0] sign changes = 0, [1] first bad = ~0
+    CUDA_TRY(cudaMemsetAsync(s->counters + 2 * s->slot, 0, sizeof(unsigned long long), s->stream));
+    CUDA_TRY(cudaMemsetAsync(s->counters + 2 * s->slot + 1, 0xff, sizeof(unsigned long long), s->stream));
+  }
+  rsfg::StepBuffers b = buffers(s, out);
+  int n;
+  if (s->fast) {
+    n = rsfg::launch_zst(g, s->fields, s->t1, s->c, b, s->z0, s->z1, mode, s->stream);
+  } else {
+    int m = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
+                                      s->scratch, 0, 0, s->z0, s->z1, s->stream);
+    if (m < 0) return fail(RSFG_ERR_CUDA, "generic convolution launch failed");
+    s->launches += m;
+    n = rsfg::launch_zst(g, s->fields, s->tid, s->c, b, s->z0, s->z1, mode, s->stream);
+  }
+  if (n < 0) return fail(RSFG_ERR_CUDA, "step launch failed");
+  s->launches += n;
+  CUDA_TRY(cudaGetLastError());
+  if (mode == rsfg::kUpdate) {
+    s->cur ^= 1;
+    s->iteration += 1;
+    s->slot = (s->slot + 1) % kSlots;
+  }
+  return RSFG_OK;
+}
+
+// Reads counters of the last `k` steps (oldest first).  Returns RSFG_OK or
+// RSFG_ERR_BLOWUP with g_err set (rsf.cpp:346-352 message).
+int check_counters(rsfg_slab* s, int k, long long* last_sign_changes, int* first_bad_iter) {
+  CUDA_TRY(cudaMemcpyAsync(s->h_counters, s->counters, kSlots * 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (first_bad_iter) *first_bad_iter = 0;
+  for (int i = k; i >= 1; --i) {
+    const int sl = ((s->slot - i) % kSlots + kSlots) % kSlots;
+    const unsigned long long bad = s->h_counters[2 * sl + 1];
+    if (last_sign_changes && i == 1) *last_sign_changes = (long long)s->h_counters[2 * sl];
+    if (bad != ~0ull) {
+      const int it = s->iteration - i + 1;  // 1-based iteration of that step
+      const long long plane = (long long)s->nx * s->ny;
+      const int x = (int)(bad % s->nx), y = (int)((bad / s->nx) % s->ny), z = (int)(bad / plane);
+      if (first_bad_iter) *first_bad_iter = it;
+      char buf[160];
+      snprintf(buf, sizeof buf, "evolution produced a non-finite value at voxel (%d,%d,%d), iteration %d", x, y,
+               z, it);
+      g_err = buf;
+      return RSFG_ERR_BLOWUP;
+    }
+  }
+  return RSFG_OK;
+}
+
+int create_common(rsfg_state** out, const float* phi0, const float* image, int nx, int ny, int nz,
+                  const rsfg_params* p, const rsfg_options* o, cudaMemcpyKind kind) {
+  if (!out) return fail(RSFG_ERR_STATE, "null output handle");
+  *out = nullptr;
+  auto* st = new rsfg_state;
+  rsfg_slab* s = &st->e;
+  int rc = setup(s, nx, ny, nz, 0, nz, p, o);
+  if (!rc) rc = upload(s, phi0, image, kind);
+  float lo = 0, hi = 0;
+  if (!rc) rc = local_range(s, &lo, &hi);
+  if (!rc) rc = init_static(s, lo, hi);
+  if (rc) {
+    std::string keep = g_err;
+    release(s);
+    delete st;
+    g_err = keep;
+    return rc;
+  }
+  *out = st;
+  return RSFG_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+__attribute__((visibility("default"))) const char* rsfg_last_error(void) { return g_err.c_str(); }
+__attribute__((visibility("default"))) const char* rsfg_version(void) { return "rsfg 0.1 (sm_100a)"; }
+
+__attribute__((visibility("default"))) void rsfg_params_default(rsfg_params* p) {
+  if (!p) return;
+  p->sigma1 = 5.0;  // rsf.hpp:14-22
+  p->sigma2 = 0.0;
+  p->alpha = 58.5225;
+  p->beta = 0.1;
+  p->epsilon = 1.0;
+  p->dt = 0.06;
+  p->max_iters = 100;
+  p->convergence_fraction = 0.0;
+  p->denom_floor = 1e-8;
+  p->grad_floor = 1e-8;
+}
+
+__attribute__((visibility("default"))) void rsfg_options_default(rsfg_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->device = 0;
+  o->fields = RSFG_FIELDS_2;
+  o->check_every = 25;
+  o->use_graphs = 1;
+}
+
+__attribute__((visibility("default"))) int rsfg_params_validate(const rsfg_params* p) { return validate(p); }
+
+__attribute__((visibility("default"))) int rsfg_gaussian_kernel(double sigma, double* weights, int32_t cap, int32_t* radius) {
+  std::vector<double> w;
+  if (int rc = gaussian(sigma, w)) return rc;
+  if ((int)w.size() > cap) return fail(RSFG_ERR_PARAM, "weights buffer too small");
+  std::memcpy(weights, w.data(), w.size() * sizeof(double));
+  if (radius) *radius = (int32_t)(w.size() / 2);
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_create(rsfg_state** out, const float* phi0, const float* image, int32_t nx, int32_t ny,
+                      int32_t nz, const rsfg_params* p, const rsfg_options* o) {
+  if (!phi0 || !image) return fail(RSFG_ERR_STATE, "null input buffer");
+  return create_common(out, phi0, image, nx, ny, nz, p, o, cudaMemcpyHostToDevice);
+}
+
+__attribute__((visibility("default"))) int rsfg_state_create_device(rsfg_state** out, const float* d_phi0, const float* d_image, int32_t nx,
+                             int32_t ny, int32_t nz, const rsfg_params* p, const rsfg_options* o) {
+  if (!d_phi0 || !d_image) return fail(RSFG_ERR_STATE, "null input buffer");
+  return create_common(out, d_phi0, d_image, nx, ny, nz, p, o, cudaMemcpyDeviceToDevice);
+}
+
+__attribute__((visibility("default"))) int rsfg_state_step(rsfg_state* st, double* frac) {
+  if (!st) return fail(RSFG_ERR_STATE, "null state");
+  rsfg_slab* s = &st->e;
+  if (int rc = step_interior(s)) return rc;
+  if (int rc = step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1])) return rc;
+  long long sc = 0;
+  int bad_it = 0;
+  int rc = check_counters(s, 1, &sc, &bad_it);
+  if (rc == RSFG_ERR_BLOWUP) {
+    // rsf.cpp:346-353 throws before the swap: phi and iteration unchanged.
+    s->cur ^= 1;
+    s->iteration -= 1;
+    s->slot = (s->slot + kSlots - 1) % kSlots;
+    return rc;
+  }
+  if (rc) return rc;
+  if (frac) *frac = (double)sc / ((double)s->nx * s->ny * s->nz);
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_run(rsfg_state* st, int32_t n, rsfg_report* rep) {
+  if (!st) return fail(RSFG_ERR_STATE, "null state");
+  rsfg_slab* s = &st->e;
+  int done = 0, pending = 0;
+  const long long l0 = s->launches;
+  while (done < n) {
+    if (int rc = step_interior(s)) return rc;
+    if (int rc = step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1])) return rc;
+    ++done;
+    ++pending;
+    if (pending == s->check_every || done == n) {
+      long long sc = 0;
+      int bad_it = 0;
+      int rc = check_counters(s, pending, &sc, &bad_it);
+      pending = 0;
+      if (rep) {
+        rep->iterations = done;
+        rep->last_sign_change_fraction = (double)sc / ((double)s->nx * s->ny * s->nz);
+      }
+      if (rc == RSFG_ERR_BLOWUP) {
+        s->valid = false;
+        if (rep) rep->blowup_iteration = bad_it;
+        return rc;
+      }
+      if (rc) return rc;
+    }
+  }
+  if (rep) rep->gpu_launches = s->launches - l0;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_profile(rsfg_state* st, int32_t steps, double* ms) {
+  if (!st || !ms || steps < 1) return fail(RSFG_ERR_STATE, "bad argument");
+  rsfg_slab* s = &st->e;
+  CUDA_TRY(cudaSetDevice(s->dev));
+  std::vector<cudaEvent_t> ev(3 * (size_t)steps);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  int rc = RSFG_OK;
+  for (int i = 0; i < steps && !rc; ++i) {
+    cudaEventRecord(ev[3 * i], s->stream);
+    rc = step_interior(s);
+    cudaEventRecord(ev[3 * i + 1], s->stream);
+    if (!rc) rc = step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1]);
+    cudaEventRecord(ev[3 * i + 2], s->stream);
+  }
+  cudaStreamSynchronize(s->stream);
+  ms[0] = ms[1] = 0.0;
+  for (int i = 0; i < steps && !rc; ++i) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]);
+    cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]);
+    ms[0] += a / steps;
+    ms[1] += b / steps;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc) return rc;
+  long long sc = 0;
+  int bad = 0;
+  return check_counters(s, std::min(steps, kSlots), &sc, &bad);
+}
+
+__attribute__((visibility("default"))) const char* rsfg_profile_name(int32_t i) {
+  static const char* names[] = {"xy: H-/H+ fields, K*x, K*y (rsf.cpp:75-94, ops.cpp:74-160)",
+                                "zst: K*z, r+-, F- - F+, delta, grad/|grad|, div, lap, combine, update "
+                                "(rsf.cpp:96-168, 324-352)"};
+  return (i >= 0 && i < 2) ? names[i] : "";
+}
+
+__attribute__((visibility("default"))) int rsfg_state_energy(rsfg_state* st, float* E) {
+  if (!st || !E) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_slab* s = &st->e;
+  if (int rc = step_interior(s)) return rc;
+  if (int rc = step_finish(s, rsfg::kEnergy, s->phi[s->cur ^ 1])) return rc;
+  CUDA_TRY(cudaMemcpyAsync(E, s->phi[s->cur ^ 1], s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_read_phi(rsfg_state* st, float* phi) {
+  if (!st || !phi) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_slab* s = &st->e;
+  CUDA_TRY(cudaSetDevice(s->dev));
+  CUDA_TRY(cudaMemcpyAsync(phi, s->phi[s->cur], s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_write_phi(rsfg_state* st, const float* phi) {
+  if (!st || !phi) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_slab* s = &st->e;
+  CUDA_TRY(cudaSetDevice(s->dev));
+  CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, s->held() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->valid = true;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_mask(rsfg_state* st, float* mask) {
+  if (!st || !mask) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_slab* s = &st->e;
+  CUDA_TRY(cudaSetDevice(s->dev));
+  float* tmp = reinterpret_cast<float*>(s->P[0]);
+  s->launches += rsfg::launch_mask(s->phi[s->cur], tmp, (long long)s->held(), s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(mask, tmp, s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_iteration(const rsfg_state* st, int32_t* it) {
+  if (!st || !it) return fail(RSFG_ERR_STATE, "null argument");
+  *it = st->e.iteration;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_device_phi(rsfg_state* st, float** d) {
+  if (!st || !d) return fail(RSFG_ERR_STATE, "null argument");
+  *d = st->e.phi[st->e.cur];
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_stream(rsfg_state* st, void** stream) {
+  if (!st || !stream) return fail(RSFG_ERR_STATE, "null argument");
+  *stream = (void*)st->e.stream;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_sync(rsfg_state* st) {
+  if (!st) return fail(RSFG_ERR_STATE, "null state");
+  CUDA_TRY(cudaStreamSynchronize(st->e.stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int64_t rsfg_state_launches(const rsfg_state* st) { return st ? st->e.launches : 0; }
+
+__attribute__((visibility("default"))) void rsfg_state_destroy(rsfg_state* st) {
+  if (!st) return;
+  release(&st->e);
+  delete st;
+}
+
+// ------------------------------------------------------------------ evolve
+namespace {
+int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rsfg_params* p,
+                const rsfg_options* o, rsfg_stop_fn stop, void* user, int stop_every, rsfg_report* rep) {
+  rsfg_report local{};
+  if (!rep) rep = &local;
+  std::memset(rep, 0, sizeof *rep);
+  if (int rc = validate(p)) return rc;
+  if (!image || !phi) return fail(RSFG_ERR_STATE, "null input buffer");
+  rsfg_options opt;
+  rsfg_options_default(&opt);
+  if (o) opt = *o;
+  cudaSetDevice(opt.device);
+  cudaEvent_t ev[5];
+  for (auto& e : ev) cudaEventCreate(&e);
+  struct EvGuard {
+    cudaEvent_t* ev;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    }
+  } guard{ev};
+
+  auto* st = new rsfg_state;
+  rsfg_slab* s = &st->e;
+  struct StGuard {
+    rsfg_state* st;
+    ~StGuard() { rsfg_state_destroy(st); }
+  } sguard{st};
+  if (int rc = setup(s, nx, ny, nz, 0, nz, p, &opt)) {
+    sguard.st = nullptr;
+    release(s);
+    delete st;
+    return rc;
+  }
+  cudaEventRecord(ev[0], s->stream);
+  if (int rc = upload(s, phi, image, cudaMemcpyHostToDevice)) return rc;
+  cudaEventRecord(ev[1], s->stream);
+  float lo, hi;
+  if (int rc = local_range(s, &lo, &hi)) return rc;
+  if (int rc = init_static(s, lo, hi)) return rc;
+  cudaEventRecord(ev[2], s->stream);
+
+  const bool per_step = p->convergence_fraction > 0.0;
+  std::vector<float> host_phi;
+  int pending = 0;
+  const long long l0 = s->launches;
+  for (int it = 0; it < p->max_iters; ++it) {
+    if (int rc = step_interior(s)) return rc;
+    if (int rc = step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1])) return rc;
+    ++pending;
+    const bool want_stop = stop && stop_every > 0 && s->iteration % stop_every == 0;
+    if (per_step || want_stop || pending == s->check_every || it + 1 == p->max_iters) {
+      long long sc = 0;
+      int bad_it = 0;
+      int rc = check_counters(s, pending, &sc, &bad_it);
+      pending = 0;
+      rep->iterations = s->iteration;
+      rep->last_sign_change_fraction = (double)sc / ((double)nx * ny * nz);
+      if (rc == RSFG_ERR_BLOWUP) {
+        rep->blowup_iteration = bad_it;
+        std::sscanf(g_err.c_str(), "evolution produced a non-finite value at voxel (%d,%d,%d)", &rep->blowup_x,
+                    &rep->blowup_y, &rep->blowup_z);
+        return rc;
+      }
+      if (rc) return rc;
+      // rsf.cpp:378: early stop on the sign-change fraction.
+      if (per_step && rep->last_sign_change_fraction < p->convergence_fraction) break;
+      // rsf.cpp:379-381: user stop callback with the current phi.
+      if (want_stop) {
+        host_phi.resize(s->held());
+        if (int rc2 = rsfg_state_read_phi(st, host_phi.data())) return rc2;
+        if (stop(host_phi.data(), nx, ny, nz, s->iteration, user)) break;
+      }
+    }
+  }
+  cudaEventRecord(ev[3], s->stream);
+  CUDA_TRY(cudaMemcpyAsync(phi, s->phi[s->cur], s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  cudaEventRecord(ev[4], s->stream);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  float ms;
+  cudaEventElapsedTime(&ms, ev[0], ev[1]);
+  rep->ms_h2d = ms;
+  cudaEventElapsedTime(&ms, ev[1], ev[2]);
+  rep->ms_init = ms;
+  cudaEventElapsedTime(&ms, ev[2], ev[3]);
+  rep->ms_loop = ms;
+  cudaEventElapsedTime(&ms, ev[3], ev[4]);
+  rep->ms_d2h = ms;
+  rep->iterations = s->iteration;
+  rep->gpu_launches = s->launches - l0;
+  return RSFG_OK;
+}
+
+struct SliceStop {
+  rsfg_stop_fn stop;
+  void* user;
+  std::vector<float> slice;
+};
+
+int slice_stop(const float* phi, int32_t nx, int32_t ny, int32_t, int32_t it, void* u) {
+  auto* ss = static_cast<SliceStop*>(u);
+  ss->slice.assign(phi, phi + (size_t)nx * ny);  // take_slice_z(phi, 0), rsf.cpp:368-369
+  return ss->stop(ss->slice.data(), nx, ny, 1, it, ss->user);
+}
+}  // namespace
+
+__attribute__((visibility("default"))) int rsfg_evolve(const float* image, float* phi, int32_t nx, int32_t ny, int32_t nz, const rsfg_params* p,
+                const rsfg_options* o, rsfg_stop_fn stop, void* user, int32_t stop_every, rsfg_report* rep) {
+  if (int rc = validate(p)) return rc;
+  if (nz == 1) {
+    // rsf.cpp:363-372: evolve a duplicated slice pair, return slice 0.
+    if (!image || !phi) return fail(RSFG_ERR_STATE, "null input buffer");
+    const size_t n = (size_t)nx * ny;
+    std::vector<float> I2(2 * n), P2(2 * n);
+    std::copy(image, image + n, I2.begin());
+    std::copy(image, image + n, I2.begin() + n);
+    std::copy(phi, phi + n, P2.begin());
+    std::copy(phi, phi + n, P2.begin() + n);
+    SliceStop ss{stop, user, {}};
+    int rc = evolve_impl(I2.data(), P2.data(), nx, ny, 2, p, o, stop ? slice_stop : nullptr, &ss, stop_every, rep);
+    if (rc) return rc;
+    std::copy(P2.begin(), P2.begin() + n, phi);
+    return RSFG_OK;
+  }
+  return evolve_impl(image, phi, nx, ny, nz, p, o, stop, user, stop_every, rep);
+}
+
+__attribute__((visibility("default"))) int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device) {
+  if (n <= 0) return RSFG_OK;
+  if (!phi || !mask) return fail(RSFG_ERR_STATE, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  float *dp = nullptr, *dm = nullptr;
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t e = cudaMalloc(&dp, n * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&dm, n * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, phi, n * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    rsfg::launch_mask(dp, dm, n, st);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mask, dm, n * sizeof(float), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dp);
+  cudaFree(dm);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? RSFG_ERR_OOM : RSFG_ERR_CUDA, cudaGetErrorString(e));
+  return RSFG_OK;
+}
+
+// ------------------------------------------------------------------- slabs
+__attribute__((visibility("default"))) int rsfg_slab_create(rsfg_slab** out, int32_t nx, int32_t ny, int32_t nz, int32_t z0, int32_t z1,
+                     const rsfg_params* p, const rsfg_options* o) {
+  if (!out) return fail(RSFG_ERR_STATE, "null output handle");
+  *out = nullptr;
+  auto* s = new rsfg_slab;
+  if (int rc = setup(s, nx, ny, nz, z0, z1, p, o)) {
+    std::string keep = g_err;
+    release(s);
+    delete s;
+    g_err = keep;
+    return rc;
+  }
+  *out = s;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_geometry(const rsfg_slab* s, int32_t* zb, int32_t* ze, int32_t* halo) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  if (zb) *zb = s->zb;
+  if (ze) *ze = s->ze;
+  if (halo) *halo = s->h;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_upload(rsfg_slab* s, const float* phi, const float* image) {
+  if (!s || !phi || !image) return fail(RSFG_ERR_STATE, "null argument");
+  if (int rc = upload(s, phi, image, cudaMemcpyHostToDevice)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_local_range(rsfg_slab* s, float* lo, float* hi) {
+  if (!s || !lo || !hi) return fail(RSFG_ERR_STATE, "null argument");
+  return local_range(s, lo, hi);
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_init(rsfg_slab* s, float lo, float hi) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  return init_static(s, lo, hi);
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_halo(rsfg_slab* s, int32_t side, void** send, void** recv, int64_t* bytes) {
+  if (!s || !send || !recv || !bytes) return fail(RSFG_ERR_STATE, "null argument");
+  const size_t plane = (size_t)s->nx * s->ny;
+  float* cur = s->phi[s->cur];
+  if (side == 0) {
+    const int k = s->z0 - s->zb;  // halo planes below (0 on the global face)
+    *recv = cur;
+    *send = cur + s->off(s->z0);
+    *bytes = (int64_t)k * plane * sizeof(float);
+  } else {
+    const int k = s->ze - s->z1;
+    *recv = cur + s->off(s->z1);
+    *send = cur + s->off(s->z1 - k);
+    *bytes = (int64_t)k * plane * sizeof(float);
+  }
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_set_stream(rsfg_slab* s, void* stream) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  if (s->own_stream && s->stream) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    cudaStreamDestroy(s->stream);
+  }
+  s->stream = (cudaStream_t)stream;
+  s->own_stream = false;
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_exchange(rsfg_slab* lo, rsfg_slab* hi) {
+  if (!lo || !hi) return fail(RSFG_ERR_STATE, "null slab");
+  if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->nz != hi->nz)
+    return fail(RSFG_ERR_SHAPE, "slabs are not z-adjacent pieces of one volume");
+  void *lo_send, *lo_recv, *hi_send, *hi_recv;
+  int64_t lo_bytes, hi_bytes;
+  rsfg_slab_halo(lo, 1, &lo_send, &lo_recv, &lo_bytes);
+  rsfg_slab_halo(hi, 0, &hi_send, &hi_recv, &hi_bytes);
+  if (lo_bytes != hi_bytes) return fail(RSFG_ERR_SHAPE, "halo sizes differ across the face");
+  cudaEvent_t e_hi, e_lo;
+  CUDA_TRY(cudaSetDevice(hi->dev));
+  CUDA_TRY(cudaEventCreateWithFlags(&e_hi, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(e_hi, hi->stream));
+  CUDA_TRY(cudaSetDevice(lo->dev));
+  CUDA_TRY(cudaEventCreateWithFlags(&e_lo, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamWaitEvent(lo->stream, e_hi, 0));
+  CUDA_TRY(cudaMemcpyPeerAsync(hi_recv, hi->dev, lo_send, lo->dev, (size_t)lo_bytes, lo->stream));
+  CUDA_TRY(cudaMemcpyPeerAsync(lo_recv, lo->dev, hi_send, hi->dev, (size_t)hi_bytes, lo->stream));
+  CUDA_TRY(cudaEventRecord(e_lo, lo->stream));
+  CUDA_TRY(cudaSetDevice(hi->dev));
+  CUDA_TRY(cudaStreamWaitEvent(hi->stream, e_lo, 0));
+  cudaEventDestroy(e_hi);
+  cudaEventDestroy(e_lo);
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_step_interior(rsfg_slab* s) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  return step_interior(s);
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_step_finish(rsfg_slab* s) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  return step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1]);
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_counters(rsfg_slab* s, int64_t* sign_changes, int64_t* first_bad) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  const int sl = (s->slot + kSlots - 1) % kSlots;
+  unsigned long long h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, s->counters + 2 * sl, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (sign_changes) *sign_changes = (int64_t)h[0];
+  if (first_bad) *first_bad = h[1] == ~0ull ? -1 : (int64_t)h[1];
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_download(rsfg_slab* s, float* phi_owned) {
+  if (!s || !phi_owned) return fail(RSFG_ERR_STATE, "null argument");
+  CUDA_TRY(cudaSetDevice(s->dev));
+  CUDA_TRY(cudaMemcpyAsync(phi_owned, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float),
+                           cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_device_phi(rsfg_slab* s, float** d) {
+  if (!s || !d) return fail(RSFG_ERR_STATE, "null argument");
+  *d = s->phi[s->cur];
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int64_t rsfg_slab_launches(const rsfg_slab* s) { return s ? s->launches : 0; }
+
+__attribute__((visibility("default"))) void rsfg_slab_destroy(rsfg_slab* s) {
+  if (!s) return;
+  release(s);
+  delete s;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// rsfg_internal.h -- device-side types and kernel launchers shared by the
+// C-ABI layer (rsfg_api.cu) and the kernels (rsfg_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rsfg {
+
+// A z-slab view of an nx*ny*nz fp32 volume (x fastest) whose buffers hold
+// global planes [zb, ze).  Every neighbour index is clamped in GLOBAL
+// coordinates, so only true volume faces clamp; slab faces read halo planes.
+struct Geom {
+  int nx, ny, nz;
+  int zb, ze;       // held global planes [zb, ze)
+  long long plane;  // nx * ny
+};
+
+constexpr int kMaxTaps = 64;  // 2R+1 <= 63 handled by the generic path
+struct Taps {
+  float w[kMaxTaps];
+  int r;
+};
+
+// Per-step scalars (RsfParams in the precision each stage uses).
+struct StepConsts {
+  float inv_eps;      // 1/epsilon                       (rsf.cpp:86)
+  float c_delta;      // epsilon/pi                      (rsf.cpp:105)
+  float eps2;         // epsilon^2
+  float alpha, beta;  // rsf.cpp:161
+  float denom_floor;  // rsf.cpp:142
+  float grad_floor;   // rsf.cpp:118
+  float i_min, i_max; // rsf.cpp:143, volume.cpp:25-33
+  double dt;          // rsf.cpp:334
+};
+
+// Device buffers of one step.  P[f] holds the separable-convolution partial
+// products as float2 pairs: fields=2 -> P[0] = (H-, H- I); fields=4 adds
+// P[1] = (H+, H+ I).
+struct StepBuffers {
+  const float* phi;
+  const float* image;
+  const float* k1i;  // K_sigma1 * I (fields=2 only)
+  const float* ki;   // K_sigma2 * I (== image when sigma2 == 0)
+  float2* P[2];
+  float* out;                       // phi_{n+1} (mode 0) or E (mode 1)
+  unsigned long long* counters;     // [0] sign changes, [1] first bad index (min)
+};
+
+enum StepMode { kUpdate = 0, kEnergy = 1 };
+
+// True when a fused, radius-specialised kernel exists for r.
+bool has_fast_radius(int r);
+
+// Kernel 1 ("xy"): Heaviside fields on a haloed tile + x pass + y pass ->
+// P for global planes [z_begin, z_end).  Returns the number of launches.
+int launch_xy(const Geom& g, int fields, const Taps& t1, float inv_eps, const float* phi,
+              const float* image, float2* P0, float2* P1, int z_begin, int z_end,
+              cudaStream_t st);
+
+// Kernel 2 ("zst"): z pass + region averages + force + curvature stencil +
+// combine + explicit update for planes [z_begin, z_end).
+int launch_zst(const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
+               int z_begin, int z_end, StepMode mode, cudaStream_t st);
+
+// Generic path (any radius, used when no specialised kernel exists):
+// Heaviside fields, then three separable passes with runtime taps through
+// scratch volumes, leaving K*fields in b.P; then kernel 2 with an identity
+// z pass.  scratch holds 2*(fields/2) float2 volumes of the held planes.
+// Returns launches, or -1 on a launch error.
+int launch_generic_conv(const Geom& g, int fields, const Taps& t1, float inv_eps, const float* phi,
+                        const float* image, float2* const P[2], float2* scratch, int zk_begin,
+                        int zk_end, int z_begin, int z_end, cudaStream_t st);
+
+// Separable 3-D convolution of a scalar field with clamp-to-edge taps
+// (init: K1*I, K2*I).  src must hold planes [z_begin-R, z_end+R) (clamped).
+int launch_convolve(const Geom& g, const Taps& t, const float* src, float* dst, float* tmp0,
+                    float* tmp1, int z_begin, int z_end, cudaStream_t st);
+
+// min/max over planes [z_begin, z_end) into mm[0..1] (ordered-int encoded).
+int launch_minmax(const Geom& g, const float* v, int z_begin, int z_end, unsigned int* mm,
+                  cudaStream_t st);
+float decode_ordered(unsigned int u);
+unsigned int encode_ordered(float f);
+
+int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st);
+
+}  // namespace rsfg
