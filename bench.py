@@ -249,7 +249,7 @@ def bench_single(args):
         dt = time.perf_counter() - t0
         if i > 0:
             e2e_times.append(dt)
-    e2e_value = nvox * ITERS_CFG / statistics.median(e2e_times)
+    e2e_value = nvox * ITERS_CFG / statistics.median(e2e_times) if e2e_times else None
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
            "iterations_per_step": ITERS_CFG, "api": "rsfg_evolve (host buffers)",
            "phase_ms": {"h2d": round(rep2.ms_h2d, 2), "init": round(rep2.ms_init, 2),

@@ -149,6 +149,25 @@ class SlabSet:
             s.close()
 
 
+def start_halo_exchange(dist, rank, world, lo_views, hi_views):
+    """Post the per-step halo sends/receives of one rank.
+
+    lo_views / hi_views = (send, recv) tensors for the face toward z=0 / z=nz-1
+    (None on a global face).  Shared by the NCCL driver and the gloo CPU tests
+    so both exercise the same pairing.  Returns the requests to wait on."""
+    ops = []
+    if rank > 0 and lo_views[0] is not None:
+        ops += [dist.P2POp(dist.isend, lo_views[0], rank - 1), dist.P2POp(dist.irecv, lo_views[1], rank - 1)]
+    if rank < world - 1 and hi_views[0] is not None:
+        ops += [dist.P2POp(dist.isend, hi_views[0], rank + 1), dist.P2POp(dist.irecv, hi_views[1], rank + 1)]
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def held_range(z0, z1, nz, halo):
+    """Planes a slab holds: [max(z0-h, 0), min(z1+h, nz)) (rsfg_slab_create)."""
+    return max(z0 - halo, 0), min(z1 + halo, nz)
+
+
 class _DevView:
     """__cuda_array_interface__ view of raw device memory (zero copy)."""
 
@@ -188,15 +207,7 @@ class DistSlab:
         return t.as_tensor(_DevView(send, n), device="cuda"), t.as_tensor(_DevView(recv, n), device="cuda")
 
     def step(self):
-        dist = self.dist
-        ops = []
-        if self.rank > 0:
-            s, r = self._views(0)
-            ops += [dist.P2POp(dist.isend, s, self.rank - 1), dist.P2POp(dist.irecv, r, self.rank - 1)]
-        if self.rank < self.world - 1:
-            s, r = self._views(1)
-            ops += [dist.P2POp(dist.isend, s, self.rank + 1), dist.P2POp(dist.irecv, r, self.rank + 1)]
-        reqs = dist.batch_isend_irecv(ops) if ops else []
+        reqs = start_halo_exchange(self.dist, self.rank, self.world, self._views(0), self._views(1))
         self.slab.step_interior()  # overlaps the exchange (no halo needed)
         for q in reqs:
             q.wait()

@@ -1,0 +1,107 @@
+"""Pin the oracle: our plain-C restatement (oracle/rsf_oracle.c) against the
+reference itself (compiled from /root/reference sources, oracle/_ref) and
+against the committed golden vectors (tests/golden/make_golden.py).
+CPU only."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from _oracle import params
+
+GOLD = Path(__file__).resolve().parent / "golden" / "rsf_golden.npz"
+TAGS = {"s3": (3.0, 0.0), "s2_15": (2.0, 1.5), "s0": (0.0, 0.0)}
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return dict(np.load(GOLD))
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a.astype(np.float64) - b) / np.maximum(1.0, np.abs(b))))
+
+
+def test_gaussian_kernel_known_answer(oracle, gold):
+    w = oracle.gaussian_kernel(3.0)
+    assert len(w) == 19  # radius ceil(3 sigma) = 9
+    assert abs(w.sum() - 1.0) < 1e-15
+    assert abs(w[9] - 0.133175996) < 1e-9
+    assert np.array_equal(w, gold["gauss_s3"])
+
+
+@pytest.mark.parametrize("tag", list(TAGS))
+def test_oracle_vs_golden(oracle, gold, tag):
+    s1, s2 = TAGS[tag]
+    p = params(sigma1=s1, sigma2=s2)
+    img, phi0 = gold["img"], gold["phi0"]
+    st = oracle.init(img, p)
+    E = oracle.energy(phi0, img, p, st)
+    assert _rel(E, gold[f"E_{tag}"]) <= 1e-6
+    phi, _, bad = oracle.step(phi0, img, p, st)
+    assert bad == -1
+    assert _rel(phi, gold[f"phi1_{tag}"]) <= 1e-6
+    for _ in range(4):
+        phi, _, _ = oracle.step(phi, img, p, st)
+    assert _rel(phi, gold[f"phi5_{tag}"]) <= 1e-5
+    # on this container's ISA the restatement reproduces the reference bit for bit
+    exact = np.array_equal(phi, gold[f"phi5_{tag}"])
+    print(f"{tag}: bit-exact={exact}")
+
+
+def test_oracle_convolution_vs_golden(oracle, gold):
+    assert _rel(oracle.convolve(gold["img"], 2.0), gold["conv_img_s2"]) <= 1e-6
+
+
+def test_oracle_bitwise_vs_reference(oracle, ref):
+    """Same host, same inputs: restatement == reference, bit for bit."""
+    from _inputs import random_case
+    img, phi = random_case(30, 26, 22, seed=4)
+    for s1, s2 in [(3.0, 0.0), (1.5, 2.0), (4.0, 0.0)]:
+        p = params(sigma1=s1, sigma2=s2)
+        st = ref.state(phi, img, p)
+        KI, KI2, lo, hi = st.static()
+        oK = oracle.init(img, p)
+        assert np.array_equal(KI, oK[0]) and np.array_equal(KI2, oK[1]) and (lo, hi) == oK[2:]
+        assert np.array_equal(st.energy(), oracle.energy(phi, img, p, oK))
+        ph = phi.copy()
+        for _ in range(3):
+            st.step()
+            ph, _, _ = oracle.step(ph, img, p, oK)
+        assert np.array_equal(st.phi(), ph)
+
+
+def test_reference_evolve_golden(ref, gold):
+    from _oracle import params as P
+    got = ref.evolve(gold["phi0"], gold["img"], P(sigma1=3.0, max_iters=10))
+    assert _rel(got, gold["evolve10_s3"]) <= 1e-5
+
+
+def test_spec_known_answers(oracle):
+    """SPEC.md acceptance checks the reference passes."""
+    n = 32
+    z, y, x = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    # #2: constant image -> zero force; plane SDF -> E = 0 in the interior
+    img = np.full((n, n, n), 77.0, np.float32)
+    phi = (x - 15.5).astype(np.float32)
+    E = oracle.energy(phi, img, params(sigma1=2.0))
+    assert np.abs(E[2:-2, 2:-2, 2:-2]).max() == 0.0
+    # #4: delta == dH/du (checked through E's delta factor on a pure force field is
+    # indirect; here: energy is finite and symmetric under x-mirroring)
+    assert np.all(np.isfinite(E))
+
+
+def test_slab_step_matches_monolithic(oracle):
+    from _inputs import random_case
+    from _oracle import Geom
+    img, phi = random_case(16, 14, 24, seed=9)
+    p = params(sigma1=2.0)
+    st = oracle.init(img, p)
+    ref, sc, _ = oracle.step(phi, img, p, st)
+    z0, z1, h = 8, 16, 6
+    zb, ze = z0 - h, z1 + h
+    g = Geom(16, 14, 24, zb, ze)
+    out, sc2, _ = oracle.step_slab(g, np.ascontiguousarray(phi[zb:ze]), np.ascontiguousarray(img[zb:ze]),
+                                   np.ascontiguousarray(st[0][zb:ze]), np.ascontiguousarray(st[1][zb:ze]),
+                                   st[2], st[3], p, z0, z1)
+    assert np.array_equal(out[z0 - zb:z1 - zb], ref[z0:z1])
