@@ -150,8 +150,8 @@ def reference_sample(img, phi0, planes):
 
 
 def run_reference(img, phi0, steps, warmup, planes):
-    from _oracle import params as ref_params
     ref = reference_lib()
+    from _oracle import params as ref_params
     ref.set_workers(0)  # all host cores (volume.cpp:18-22)
     si, sp = reference_sample(img, phi0, planes)
     st = ref.state(sp, si, ref_params(sigma1=SIGMA1, sigma2=0.0))
