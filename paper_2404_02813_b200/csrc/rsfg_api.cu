@@ -4,11 +4,14 @@
 // One engine type serves both the monolithic state (rsf::init_evolution /
 // evolve_step, rsf.cpp:293-357) and z-slabs: a state is the
 // slab [0, nz) with no halo.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -108,6 +111,7 @@ struct rsfg_slab {
   unsigned long long* counters = nullptr;   // device [kSlots][2]
   unsigned long long* h_counters = nullptr; // pinned mirror
   unsigned int* mm = nullptr;               // device min/max scratch
+  rsfg::XYMaps xymaps[2] = {};              // TMA maps for kernel 1, per phi buffer
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -150,6 +154,40 @@ void release(rsfg_slab* s) {
   cudaFree(s->mm);
   if (s->h_counters) cudaFreeHost(s->h_counters);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+// TMA descriptors for kernel 1's tiles (3-D fp32 maps of the held planes).
+// Needs 16-byte row pitch (nx % 4 == 0); otherwise kernel 1 uses LDG.
+void make_xy_maps(rsfg_slab* s) {
+  s->xymaps[0].valid = s->xymaps[1].valid = false;
+  int bx = 0, by = 0;
+  const char* off = std::getenv("RSFG_NO_TMA");
+  if ((off && off[0] == '1') || !s->fast || (s->nx % 4) != 0 || !rsfg::xy_tma_box(s->t1.r, &bx, &by)) return;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+      return;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  auto encode = [&](CUtensorMap* m, const float* ptr) {
+    const cuuint64_t dims[3] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny, (cuuint64_t)(s->ze - s->zb)};
+    const cuuint64_t strides[2] = {(cuuint64_t)s->nx * 4, (cuuint64_t)s->nx * s->ny * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  CUtensorMap img;
+  if (!encode(&img, s->image)) return;
+  for (int b = 0; b < 2; ++b) {
+    if (!encode(&s->xymaps[b].phi, s->phi[b])) return;
+    s->xymaps[b].img = img;
+  }
+  s->xymaps[0].valid = s->xymaps[1].valid = true;
 }
 
 int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_params* p,
@@ -195,6 +233,8 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   s->c.denom_floor = (float)p->denom_floor;
   s->c.grad_floor = (float)p->grad_floor;
   s->c.dt = p->dt;
+  s->c.dt_f = (float)p->dt;
+  s->c.inv_grad_floor = (float)(1.0 / p->grad_floor);
 
   CUDA_TRY(cudaSetDevice(s->dev));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
@@ -214,6 +254,7 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
+  make_xy_maps(s);
   // Never-read halo planes must still be finite memory: zero everything once.
   CUDA_TRY(cudaMemsetAsync(s->phi[0], 0, held * sizeof(float), s->stream));
   CUDA_TRY(cudaMemsetAsync(s->phi[1], 0, held * sizeof(float), s->stream));
@@ -294,7 +335,7 @@ int xy_planes(rsfg_slab* s, int a, int b) {
   int n;
   if (s->fast) {
     n = rsfg::launch_xy(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P[0], s->P[1], a, b,
-                        s->stream);
+                        &s->xymaps[s->cur], s->stream);
   } else {
     n = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
                                   s->scratch, a, b, 0, 0, s->stream);

@@ -1,0 +1,114 @@
+// rsfg_device.cuh -- device helpers shared by the sm_100a kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "rsfg_internal.h"
+
+// Radii with a specialised (register-window) kernel; others take the generic path.
+#define RSFG_RADII(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(15) X(18)
+
+namespace rsfg {
+namespace {
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+__device__ __forceinline__ size_t vidx(const Geom& g, int x, int y, int z) {
+  return (size_t)(z - g.zb) * (size_t)g.plane + (size_t)y * (size_t)g.nx + (size_t)x;
+}
+
+// Packed two-lane FP32 FMA (sm_100 FFMA2): acc + w * v on both lanes.
+__device__ __forceinline__ float2 ffma2(float w, float2 v, float2 acc) {
+  float2 d;
+  asm("{\n\t.reg .b64 wv, vv, av, dv;\n\t"
+      "mov.b64 wv, {%2, %2};\n\t"
+      "mov.b64 vv, {%3, %4};\n\t"
+      "mov.b64 av, {%5, %6};\n\t"
+      "fma.rn.f32x2 dv, wv, vv, av;\n\t"
+      "mov.b64 {%0, %1}, dv;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(w), "f"(v.x), "f"(v.y), "f"(acc.x), "f"(acc.y));
+  return d;
+}
+
+__device__ __forceinline__ float2 fmul2(float w, float2 v) { return make_float2(w * v.x, w * v.y); }
+
+// atan(q)/pi for q in [0, 1]: q * P(q^2), degree-8 fit; max relative error
+// 1.9e-7 in fp32 (CUDA's atanf is 2 ulp); 9 FMAs, no branches.
+__device__ __forceinline__ float atan_over_pi(float q) {
+  const float x = q * q;
+  float p = 0.000906360219232738f;
+  p = fmaf(p, x, -0.00511184660717845f);
+  p = fmaf(p, x, 0.013584661297500134f);
+  p = fmaf(p, x, -0.023883428424596786f);
+  p = fmaf(p, x, 0.0338696613907814f);
+  p = fmaf(p, x, -0.04521126672625542f);
+  p = fmaf(p, x, 0.06363844871520996f);
+  p = fmaf(p, x, -0.10610246658325195f);
+  p = fmaf(p, x, 0.31830987334251404f);
+  return p * q;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Smoothed step H+ = 1/2 [1 + (2/pi) atan(phi/eps)] and H- = 1 - H+
+// (rsf.cpp:22-25, 89-90).  The side that is small is always evaluated
+// directly (atan(1/t)/pi for t > 1) so both values keep full relative
+// precision in fp32, as the reference's f64 evaluation does.
+__device__ __forceinline__ void heaviside_pair(float phi, float inv_eps, float& hm, float& hp) {
+  const float u = phi * inv_eps;
+  const float t = fabsf(u);
+  const bool far = t > 1.0f;
+  const float a = atan_over_pi(far ? rcp_approx(t) : t);
+  const float small = far ? a : 0.5f - a;
+  const float big = far ? 1.0f - a : 0.5f + a;
+  const bool pos = u >= 0.0f;
+  hm = pos ? small : big;
+  hp = pos ? big : small;
+}
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier, sm_90+/sm_100a PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+}  // namespace rsfg

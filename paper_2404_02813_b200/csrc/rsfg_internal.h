@@ -2,6 +2,7 @@
 // C-ABI layer (rsfg_api.cu) and the kernels (rsfg_kernels.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,8 +31,10 @@ struct StepConsts {
   float alpha, beta;  // rsf.cpp:161
   float denom_floor;  // rsf.cpp:142
   float grad_floor;   // rsf.cpp:118
+  float inv_grad_floor;  // 1 / grad_floor
   float i_min, i_max; // rsf.cpp:143, volume.cpp:25-33
   double dt;          // rsf.cpp:334
+  float dt_f;
 };
 
 // Device buffers of one step.  P[f] holds the separable-convolution partial
@@ -52,11 +55,23 @@ enum StepMode { kUpdate = 0, kEnergy = 1 };
 // True when a fused, radius-specialised kernel exists for r.
 bool has_fast_radius(int r);
 
+// TMA descriptors of kernel 1's input tiles (3-D fp32 maps of the held
+// planes, box = xy_tma_box(R)).  valid == false -> LDG loads.
+struct XYMaps {
+  CUtensorMap phi;
+  CUtensorMap img;
+  bool valid;
+};
+
+// Box (x, y) of kernel 1's haloed input tile for radius r; false if no
+// specialised kernel exists.
+bool xy_tma_box(int r, int* bx, int* by);
+
 // Kernel 1 ("xy"): Heaviside fields on a haloed tile + x pass + y pass ->
 // P for global planes [z_begin, z_end).  Returns the number of launches.
 int launch_xy(const Geom& g, int fields, const Taps& t1, float inv_eps, const float* phi,
               const float* image, float2* P0, float2* P1, int z_begin, int z_end,
-              cudaStream_t st);
+              const XYMaps* maps, cudaStream_t st);
 
 // Kernel 2 ("zst"): z pass + region averages + force + curvature stencil +
 // combine + explicit update for planes [z_begin, z_end).
