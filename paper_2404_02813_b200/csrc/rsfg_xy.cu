@@ -3,8 +3,8 @@
 // separable Gaussian (reference rsf.cpp:75-94, ops.cpp:74-160).
 //
 // The (TX+2R) x (TY+2R) phi and I tiles arrive by TMA (cp.async.bulk.tensor,
-// one elected thread, mbarrier completion; out-of-volume elements are
-// zero-filled and replaced by clamp-to-edge reads of the tile) when the row
+// one thread, mbarrier completion; edge tiles read their clamp-to-edge
+// neighbours from inside the box) when the row
 // pitch allows it (nx % 4 == 0), else by batched LDG.
 #include "rsfg_device.cuh"
 
@@ -21,7 +21,8 @@ struct XYCfg {
   static constexpr int QX = TX | 1;
   static constexpr size_t kHsBytes = ((size_t)NP * WY * PX * sizeof(float2) + 127) & ~(size_t)127;
   static constexpr size_t kXsBytes = (size_t)NP * WY * QX * sizeof(float2);
-  static constexpr size_t kRawBytes = 2 * (size_t)BOXX * WY * sizeof(float);  // phi + I tiles (TMA)
+  static constexpr size_t kTileBytes = ((size_t)BOXX * WY * sizeof(float) + 127) & ~(size_t)127;
+  static constexpr size_t kRawBytes = 2 * kTileBytes;  // phi + I tiles (TMA dst: 128-byte aligned)
   static constexpr size_t kUnion = kXsBytes > kRawBytes ? kXsBytes : kRawBytes;
   static constexpr size_t kSmem = kHsBytes + kUnion + 16;  // + mbarrier
   static constexpr int kThreads = 256;
@@ -40,30 +41,31 @@ __global__ void __launch_bounds__(256) xy_kernel(Geom g, Taps taps, float inv_ep
   float2* Hs = reinterpret_cast<float2*>(smem_raw);                 // [NP][WY][PX]
   float2* Xs = reinterpret_cast<float2*>(smem_raw + C::kHsBytes);   // [NP][WY][QX]
   float* Tphi = reinterpret_cast<float*>(smem_raw + C::kHsBytes);   // [WY][BOXX] (aliases Xs)
-  float* Timg = Tphi + C::BOXX * C::WY;
+  float* Timg = reinterpret_cast<float*>(smem_raw + C::kHsBytes + C::kTileBytes);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + C::kHsBytes + C::kUnion);
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, z = z_begin + blockIdx.z;
 
   // Phase A: the haloed tile, then the Heaviside fields once per loaded voxel.
   if constexpr (TMA) {
+    // The box starts at max(origin, 0): TMA fills positive out-of-range
+    // elements with zeros; the clamped read below never touches them.
+    const int bx0 = max(x0 - R, 0), by0 = max(y0 - R, 0);
     if (threadIdx.x == 0) {
       mbar_init(bar, 1);
-      mbar_expect_tx(bar, (uint32_t)C::kRawBytes);
-      tma_load_3d(Tphi, &map_phi, bar, x0 - R, y0 - R, z - g.zb);
-      tma_load_3d(Timg, &map_img, bar, x0 - R, y0 - R, z - g.zb);
+      mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
+      tma_load_3d(Tphi, &map_phi, bar, bx0, by0, z - g.zb);
+      tma_load_3d(Timg, &map_img, bar, bx0, by0, z - g.zb);
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(bar, 0);
-    // Interior tiles read the tile as is; edge tiles read the clamped element
-    // (TMA zero-fills outside the volume).
     const bool edge = x0 - R < 0 || y0 - R < 0 || x0 - R + C::WX > g.nx || y0 - R + C::WY > g.ny;
 #pragma unroll 4
     for (int e = threadIdx.x; e < C::WX * C::WY; e += C::kThreads) {
       const int ey = e / C::WX, ex = e - ey * C::WX;
       int src = ey * C::BOXX + ex;
-      if (edge) {
-        const int cx = clampi(x0 - R + ex, 0, g.nx - 1) - (x0 - R);
-        const int cy = clampi(y0 - R + ey, 0, g.ny - 1) - (y0 - R);
+      if (edge) {  // clamp-to-edge in global coordinates, then into the box
+        const int cx = clampi(x0 - R + ex, 0, g.nx - 1) - bx0;
+        const int cy = clampi(y0 - R + ey, 0, g.ny - 1) - by0;
         src = cy * C::BOXX + cx;
       }
       const float p = Tphi[src], im = Timg[src];

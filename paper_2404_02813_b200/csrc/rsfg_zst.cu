@@ -8,7 +8,7 @@ namespace {
 
 // ---------------------------------------------------------------- kernel 2
 // One CTA = TX x TY columns x (TZC * NCH) planes, streamed in z.  Shared
-// memory holds a 5-plane ring of phi (halo 2 in x/y), a 3-plane ring of the
+// memory holds a 6-plane ring of phi (halo 2 in x/y), a 3-plane ring of the
 // normalized gradient (halo 1) and the z-pass results of one TZC chunk.
 template <int R, int NP, int TX, int TY, int TZC, int NCH>
 struct ZCfg {
@@ -19,7 +19,7 @@ struct ZCfg {
   static constexpr int kPhiPer = (FPL + kThreads - 1) / kThreads;
   static constexpr int TZ = TZC * NCH;
   static constexpr size_t kSmem =
-      (size_t)(5 * FPL + 3 * 3 * NPL) * sizeof(float) + (size_t)NP * TZC * TX * TY * sizeof(float2);
+      (size_t)(6 * FPL + 3 * 3 * NPL) * sizeof(float) + (size_t)NP * TZC * TX * TY * sizeof(float2);
 };
 
 template <int R, int NP, int TX, int TY, int TZC, int NCH>
@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(TX* TY, 2)
     zst_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end, int mode) {
   using C = ZCfg<R, NP, TX, TY, TZC, NCH>;
   extern __shared__ float smemf[];
-  float* Phi = smemf;                   // [5][FY][FX] ring, slot = (q - (z0-2)) % 5
-  float* Nr = Phi + 5 * C::FPL;         // [3 slots][3 comps][NYr][NXr]
+  float* Phi = smemf;                   // [6][FY][FX] ring, slot = (q - (z0-2)) % 6
+  float* Nr = Phi + 6 * C::FPL;         // [3 slots][3 comps][NYr][NXr]
   float2* KH = reinterpret_cast<float2*>(Nr + 9 * C::NPL);  // [NP][TZC][TY*TX]
   __shared__ unsigned int s_count;
 
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(TX* TY, 2)
   }
   auto plane_ptr = [&](int q) { return b.phi + (size_t)(clampi(q, g.zb, g.ze - 1) - g.zb) * (size_t)plane; };
   // ring slot of global plane q (used outside the steady-state loop only)
-  auto slot_of = [&](int q) { return ((q - (z0 - 2)) % 5) * C::FPL; };
+  auto slot_of = [&](int q) { return ((q - (z0 - 2)) % 6) * C::FPL; };
 
   // normal positions: own column (i = tx+1, j = ty+1) and, for tid < kHalo,
   // one halo position of the (TX+2) x (TY+2) ring.
@@ -125,17 +125,19 @@ __global__ void __launch_bounds__(TX* TY, 2)
   const int col = min(y, ny - 1) * nx + min(x, nx - 1);
   unsigned int my_count = 0;
 
-  // ---- prologue: phi planes z0-2 .. z0+2 into ring slots 0..4
+  // ---- prologue: phi planes z0-2 .. z0+3 into ring slots 0..5
 #pragma unroll 1
-  for (int q = z0 - 2; q <= z0 + 2; ++q) {
+  for (int q = z0 - 2; q <= z0 + 3; ++q) {
     const float* src = plane_ptr(q);
     float* dst = Phi + slot_of(q);
 #pragma unroll
     for (int k = 0; k < C::kPhiPer; ++k)
       if (phi_s[k] >= 0) dst[phi_s[k]] = __ldg(src + phi_g[k]);
   }
-  // rotating ring offsets: planes zo-2 .. zo+2 (phi), zo-1 / zo / free (normals)
-  int o_m2 = 0, o_m1 = C::FPL, o_0 = 2 * C::FPL, o_p1 = 3 * C::FPL, o_p2 = 4 * C::FPL;
+  // rotating ring offsets: planes zo-2 .. zo+3 (phi), zo-1 / zo / free (normals).
+  // The plane refilled during step zo (zo+4, into zo-2's slot) is first read
+  // two steps later, so the two barriers per step order every ring access.
+  int o_m2 = 0, o_m1 = C::FPL, o_0 = 2 * C::FPL, o_p1 = 3 * C::FPL, o_p2 = 4 * C::FPL, o_p3 = 5 * C::FPL;
   float* n_m = Nr;
   float* n_0 = Nr + 3 * C::NPL;
   float* n_f = Nr + 6 * C::NPL;
@@ -185,10 +187,10 @@ __global__ void __launch_bounds__(TX* TY, 2)
 #pragma unroll 1
     for (int t = 0; t < tend; ++t) {
       const int zo = zc + t;
-      // prefetch: phi plane zo+3 (ring refill) and the static fields at zo+1
+      // prefetch: phi plane zo+4 (ring refill) and the static fields at zo+1
       float nxt[C::kPhiPer];
       {
-        const float* src = plane_ptr(zo + 3);
+        const float* src = plane_ptr(zo + 4);
 #pragma unroll
         for (int k = 0; k < C::kPhiPer; ++k) nxt[k] = phi_s[k] >= 0 ? __ldg(src + phi_g[k]) : 0.0f;
       }
@@ -252,19 +254,20 @@ __global__ void __launch_bounds__(TX* TY, 2)
           }
         }
       }
-      __syncthreads();
       {
-        float* dst = Phi + o_m2;  // plane zo-2 is no longer read: refill with zo+3
+        float* dst = Phi + o_m2;  // plane zo-2 is not read in this step: refill with zo+4
 #pragma unroll
         for (int k = 0; k < C::kPhiPer; ++k)
           if (phi_s[k] >= 0) dst[phi_s[k]] = nxt[k];
       }
+      __syncthreads();
       const int ot = o_m2;
       o_m2 = o_m1;
       o_m1 = o_0;
       o_0 = o_p1;
       o_p1 = o_p2;
-      o_p2 = ot;
+      o_p2 = o_p3;
+      o_p3 = ot;
       float* nt = n_m;
       n_m = n_0;
       n_0 = n_f;

@@ -179,3 +179,26 @@ def test_cfg1_full_run_P3(rsf, oracle, fields):
     assert close.mean() >= 0.995
     # Dice vs ground truth comparable to the reference's own (0.9699 with seeded phi0)
     assert abs(rsf.dice(m_got, gt) - rsf.dice(m_ref, gt)) < 1e-3
+
+
+@pytest.mark.parametrize("sigma1", [0.0, 1.0, 3.0, 6.0])
+@pytest.mark.parametrize("fields", [2, 4])
+def test_tma_and_ldg_paths_bitwise(rsf, sigma1, fields, monkeypatch):
+    """Kernel 1 loads its tile by TMA when nx % 4 == 0, else by LDG: same bits."""
+    img, phi, _ = case(40, 36, 32)
+    p = _params(rsf, sigma1=sigma1, max_iters=3)
+    a = rsf.evolve(phi, img, p, fields=fields)
+    monkeypatch.setenv("RSFG_NO_TMA", "1")
+    b = rsf.evolve(phi, img, p, fields=fields)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("fields", [2, 4])
+def test_repeat_runs_bitwise(rsf, fields):
+    """Many CTAs streaming long z-ranges: repeated runs must agree bit for bit
+    (catches shared-memory ring races)."""
+    img, phi, _ = case(64, 48, 150, n_branches=4)
+    p = _params(rsf, sigma1=2.0, max_iters=4)
+    ref = rsf.evolve(phi, img, p, fields=fields)
+    for _ in range(3):
+        assert np.array_equal(rsf.evolve(phi, img, p, fields=fields), ref)
