@@ -65,8 +65,11 @@ typedef struct rsfg_options {
   int32_t device;      /* CUDA device ordinal (default 0)                               */
   int32_t fields;      /* RSFG_FIELDS_2 or RSFG_FIELDS_4 (default: RSFG_FIELDS_2)      */
   int32_t check_every; /* evolve/run: host checks blowup every N steps (default 25)     */
-  int32_t use_graphs;  /* capture per-step launches in CUDA graphs (default 1)          */
-  int32_t reserved[4];
+  int32_t use_graphs;  /* reserved: per-step launches are plain stream launches          */
+  int32_t reuse_workspace; /* rsfg_evolve keeps its device buffers for the calling thread's
+                              next call of the same shape (default 1); see
+                              rsfg_release_workspace()                                  */
+  int32_t reserved[3];
 } rsfg_options;
 
 typedef struct rsfg_report {
@@ -99,6 +102,9 @@ int rsfg_gaussian_kernel(double sigma, double* weights, int32_t cap, int32_t* ra
 int rsfg_evolve(const float* image, float* phi_inout, int32_t nx, int32_t ny, int32_t nz,
                 const rsfg_params* p, const rsfg_options* o, rsfg_stop_fn stop, void* user,
                 int32_t stop_every, rsfg_report* report);
+
+/* Frees the calling thread's cached rsfg_evolve workspace (if any). */
+void rsfg_release_workspace(void);
 
 /* rsf::extract_mask (rsf.cpp:386-396): mask = phi < 0 ? 1 : 0, on the GPU. */
 int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device);

@@ -44,7 +44,8 @@ class rsfg_options(C.Structure):
         ("fields", C.c_int32),
         ("check_every", C.c_int32),
         ("use_graphs", C.c_int32),
-        ("reserved", C.c_int32 * 4),
+        ("reuse_workspace", C.c_int32),
+        ("reserved", C.c_int32 * 3),
     ]
 
 
@@ -104,6 +105,7 @@ SIGNATURES = {
     "rsfg_evolve": (C.c_int, [FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options), STOP_FN, VP, I32,
                               P(rsfg_report)]),
     "rsfg_extract_mask": (C.c_int, [FP, FP, C.c_int64, I32]),
+    "rsfg_release_workspace": (None, []),
     "rsfg_state_create": (C.c_int, [P(VP), FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options)]),
     "rsfg_state_create_device": (C.c_int, [P(VP), FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options)]),
     "rsfg_state_step": (C.c_int, [VP, P(C.c_double)]),

@@ -138,6 +138,10 @@ struct rsfg_state {
 };
 
 namespace {
+thread_local rsfg_state* t_cache = nullptr;  // rsfg_evolve workspace of this thread
+}
+
+namespace {
 
 void release(rsfg_slab* s) {
   if (!s) return;
@@ -161,8 +165,11 @@ void release(rsfg_slab* s) {
 void make_xy_maps(rsfg_slab* s) {
   s->xymaps[0].valid = s->xymaps[1].valid = false;
   int bx = 0, by = 0;
-  const char* off = std::getenv("RSFG_NO_TMA");
-  if ((off && off[0] == '1') || !s->fast || (s->nx % 4) != 0 || !rsfg::xy_tma_box(s->t1.r, &bx, &by)) return;
+  // Opt-in: measured on B200 the single-shot TMA tile is not faster than the
+  // batched-LDG prologue at 512^3 (profiles/r01_tma_vs_ldg.txt); kept for the
+  // z-pipelined variant.
+  const char* on = std::getenv("RSFG_TMA");
+  if (!(on && on[0] == '1') || !s->fast || (s->nx % 4) != 0 || !rsfg::xy_tma_box(s->t1.r, &bx, &by)) return;
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -258,6 +265,30 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   // Never-read halo planes must still be finite memory: zero everything once.
   CUDA_TRY(cudaMemsetAsync(s->phi[0], 0, held * sizeof(float), s->stream));
   CUDA_TRY(cudaMemsetAsync(s->phi[1], 0, held * sizeof(float), s->stream));
+  return RSFG_OK;
+}
+
+// New parameters on an existing workspace of the same shape and radii.
+int reconfigure(rsfg_slab* s, const rsfg_params* p, const rsfg_options* o) {
+  if (int rc = validate(p)) return rc;
+  s->p = *p;
+  s->check_every = std::min(std::max(o->check_every, 1), kSlots);
+  const double eps = p->epsilon;
+  s->c.inv_eps = (float)(1.0 / eps);
+  s->c.c_delta = (float)((1.0 / M_PI) * eps);
+  s->c.eps2 = (float)(eps * eps);
+  s->c.alpha = (float)p->alpha;
+  s->c.beta = (float)p->beta;
+  s->c.denom_floor = (float)p->denom_floor;
+  s->c.grad_floor = (float)p->grad_floor;
+  s->c.inv_grad_floor = (float)(1.0 / p->grad_floor);
+  s->c.dt = p->dt;
+  s->c.dt_f = (float)p->dt;
+  s->cur = 0;
+  s->slot = 0;
+  s->iteration = 0;
+  s->valid = true;
+  s->initialized = false;
   return RSFG_OK;
 }
 
@@ -465,6 +496,7 @@ __attribute__((visibility("default"))) void rsfg_options_default(rsfg_options* o
   o->fields = RSFG_FIELDS_2;
   o->check_every = 25;
   o->use_graphs = 1;
+  o->reuse_workspace = 1;
 }
 
 __attribute__((visibility("default"))) int rsfg_params_validate(const rsfg_params* p) { return validate(p); }
@@ -673,18 +705,46 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
     }
   } guard{ev};
 
-  auto* st = new rsfg_state;
+  // Workspace reuse: the last evolve's device buffers stay with the calling
+  // thread and serve the next call of the same shape/radii (no cudaMalloc,
+  // stream or pinned-buffer setup on the hot e2e path).
+  rsfg_state* st = nullptr;
+  if (opt.reuse_workspace && t_cache) {
+    rsfg_slab* c = &t_cache->e;
+    if (c->dev == opt.device && c->nx == nx && c->ny == ny && c->nz == nz && c->fields == opt.fields &&
+        c->p.sigma1 == p->sigma1 && c->p.sigma2 == p->sigma2) {
+      st = t_cache;
+      t_cache = nullptr;
+      if (int rc = reconfigure(c, p, &opt)) {
+        rsfg_state_destroy(st);
+        return rc;
+      }
+    } else {
+      rsfg_state_destroy(t_cache);
+      t_cache = nullptr;
+    }
+  }
+  if (!st) {
+    st = new rsfg_state;
+    if (int rc = setup(&st->e, nx, ny, nz, 0, nz, p, &opt)) {
+      release(&st->e);
+      delete st;
+      return rc;
+    }
+  }
   rsfg_slab* s = &st->e;
   struct StGuard {
     rsfg_state* st;
-    ~StGuard() { rsfg_state_destroy(st); }
-  } sguard{st};
-  if (int rc = setup(s, nx, ny, nz, 0, nz, p, &opt)) {
-    sguard.st = nullptr;
-    release(s);
-    delete st;
-    return rc;
-  }
+    bool keep;
+    ~StGuard() {
+      if (keep && st->e.valid) {
+        if (t_cache) rsfg_state_destroy(t_cache);
+        t_cache = st;
+      } else {
+        rsfg_state_destroy(st);
+      }
+    }
+  } sguard{st, opt.reuse_workspace != 0};
   cudaEventRecord(ev[0], s->stream);
   if (int rc = upload(s, phi, image, cudaMemcpyHostToDevice)) return rc;
   cudaEventRecord(ev[1], s->stream);
@@ -776,6 +836,11 @@ __attribute__((visibility("default"))) int rsfg_evolve(const float* image, float
     return RSFG_OK;
   }
   return evolve_impl(image, phi, nx, ny, nz, p, o, stop, user, stop_every, rep);
+}
+
+__attribute__((visibility("default"))) void rsfg_release_workspace(void) {
+  rsfg_state_destroy(t_cache);
+  t_cache = nullptr;
 }
 
 __attribute__((visibility("default"))) int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device) {

@@ -16,7 +16,9 @@ template <int R, int NP, int TX, int TY, int BX, int BY>
 struct XYCfg {
   static constexpr int WX = TX + 2 * R;
   static constexpr int WY = TY + 2 * R;
-  static constexpr int BOXX = (WX + 3) & ~3;  // TMA box row: multiple of 16 bytes
+  // TMA box row: starts on a 16-byte boundary (x origin rounded down to a
+  // multiple of 4 floats) and spans a multiple of 16 bytes.
+  static constexpr int BOXX = (WX + 3 + 3) & ~3;
   static constexpr int PX = WX | 1;  // odd pitch (float2): conflict-free row-strided LDS.64
   static constexpr int QX = TX | 1;
   static constexpr size_t kHsBytes = ((size_t)NP * WY * PX * sizeof(float2) + 127) & ~(size_t)127;
@@ -47,9 +49,10 @@ __global__ void __launch_bounds__(256) xy_kernel(Geom g, Taps taps, float inv_ep
 
   // Phase A: the haloed tile, then the Heaviside fields once per loaded voxel.
   if constexpr (TMA) {
-    // The box starts at max(origin, 0): TMA fills positive out-of-range
-    // elements with zeros; the clamped read below never touches them.
-    const int bx0 = max(x0 - R, 0), by0 = max(y0 - R, 0);
+    // The box starts at max(origin, 0) rounded down to 16 bytes (TMA faults on
+    // negative or unaligned x starts here); positive out-of-range elements are
+    // zero-filled and never read: edge tiles read their clamped neighbour.
+    const int bx0 = max(x0 - R, 0) & ~3, by0 = max(y0 - R, 0);
     if (threadIdx.x == 0) {
       mbar_init(bar, 1);
       mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
@@ -59,10 +62,11 @@ __global__ void __launch_bounds__(256) xy_kernel(Geom g, Taps taps, float inv_ep
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(bar, 0);
     const bool edge = x0 - R < 0 || y0 - R < 0 || x0 - R + C::WX > g.nx || y0 - R + C::WY > g.ny;
+    const int shift = (x0 - R) - bx0;  // 0..3 on interior tiles
 #pragma unroll 4
     for (int e = threadIdx.x; e < C::WX * C::WY; e += C::kThreads) {
       const int ey = e / C::WX, ex = e - ey * C::WX;
-      int src = ey * C::BOXX + ex;
+      int src = ey * C::BOXX + ex + shift;
       if (edge) {  // clamp-to-edge in global coordinates, then into the box
         const int cx = clampi(x0 - R + ex, 0, g.nx - 1) - bx0;
         const int cy = clampi(y0 - R + ey, 0, g.ny - 1) - by0;

@@ -8,8 +8,9 @@ namespace {
 
 // ---------------------------------------------------------------- kernel 2
 // One CTA = TX x TY columns x (TZC * NCH) planes, streamed in z.  Shared
-// memory holds a 6-plane ring of phi (halo 2 in x/y), a 3-plane ring of the
-// normalized gradient (halo 1) and the z-pass results of one TZC chunk.
+// memory holds a 7-plane ring of phi (halo 2 in x/y), a 4-plane ring of the
+// normalized gradient (halo 1) and the z-pass results of one TZC chunk.  The
+// ring depths let one barrier per plane order every ring access.
 template <int R, int NP, int TX, int TY, int TZC, int NCH>
 struct ZCfg {
   static constexpr int FX = TX + 4, FY = TY + 4, FPL = FX * FY;  // phi plane with halo 2
@@ -19,7 +20,7 @@ struct ZCfg {
   static constexpr int kPhiPer = (FPL + kThreads - 1) / kThreads;
   static constexpr int TZ = TZC * NCH;
   static constexpr size_t kSmem =
-      (size_t)(6 * FPL + 3 * 3 * NPL) * sizeof(float) + (size_t)NP * TZC * TX * TY * sizeof(float2);
+      (size_t)(7 * FPL + 4 * 3 * NPL) * sizeof(float) + (size_t)NP * TZC * TX * TY * sizeof(float2);
 };
 
 template <int R, int NP, int TX, int TY, int TZC, int NCH>
@@ -27,9 +28,9 @@ __global__ void __launch_bounds__(TX* TY, 2)
     zst_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end, int mode) {
   using C = ZCfg<R, NP, TX, TY, TZC, NCH>;
   extern __shared__ float smemf[];
-  float* Phi = smemf;                   // [6][FY][FX] ring, slot = (q - (z0-2)) % 6
-  float* Nr = Phi + 6 * C::FPL;         // [3 slots][3 comps][NYr][NXr]
-  float2* KH = reinterpret_cast<float2*>(Nr + 9 * C::NPL);  // [NP][TZC][TY*TX]
+  float* Phi = smemf;                   // [7][FY][FX] ring, slot = (q - (z0-2)) % 7
+  float* Nr = Phi + 7 * C::FPL;         // [4 slots][3 comps][NYr][NXr]
+  float2* KH = reinterpret_cast<float2*>(Nr + 12 * C::NPL);  // [NP][TZC][TY*TX]
   __shared__ unsigned int s_count;
 
   const int tid = threadIdx.x;
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(TX* TY, 2)
   }
   auto plane_ptr = [&](int q) { return b.phi + (size_t)(clampi(q, g.zb, g.ze - 1) - g.zb) * (size_t)plane; };
   // ring slot of global plane q (used outside the steady-state loop only)
-  auto slot_of = [&](int q) { return ((q - (z0 - 2)) % 6) * C::FPL; };
+  auto slot_of = [&](int q) { return ((q - (z0 - 2)) % 7) * C::FPL; };
 
   // normal positions: own column (i = tx+1, j = ty+1) and, for tid < kHalo,
   // one halo position of the (TX+2) x (TY+2) ring.
@@ -125,25 +126,30 @@ __global__ void __launch_bounds__(TX* TY, 2)
   const int col = min(y, ny - 1) * nx + min(x, nx - 1);
   unsigned int my_count = 0;
 
-  // ---- prologue: phi planes z0-2 .. z0+3 into ring slots 0..5
+  // ---- prologue: phi planes z0-2 .. z0+4 into ring slots 0..6
 #pragma unroll 1
-  for (int q = z0 - 2; q <= z0 + 3; ++q) {
+  for (int q = z0 - 2; q <= z0 + 4; ++q) {
     const float* src = plane_ptr(q);
     float* dst = Phi + slot_of(q);
 #pragma unroll
     for (int k = 0; k < C::kPhiPer; ++k)
       if (phi_s[k] >= 0) dst[phi_s[k]] = __ldg(src + phi_g[k]);
   }
-  // rotating ring offsets: planes zo-2 .. zo+3 (phi), zo-1 / zo / free (normals).
-  // The plane refilled during step zo (zo+4, into zo-2's slot) is first read
-  // two steps later, so the two barriers per step order every ring access.
-  int o_m2 = 0, o_m1 = C::FPL, o_0 = 2 * C::FPL, o_p1 = 3 * C::FPL, o_p2 = 4 * C::FPL, o_p3 = 5 * C::FPL;
-  float* n_m = Nr;
-  float* n_0 = Nr + 3 * C::NPL;
-  float* n_f = Nr + 6 * C::NPL;
+  // Rotating ring offsets, phi planes zo-2 .. zo+4 and normal planes
+  // zo-2 / zo-1 / zo / free.  Per step: write normal plane zo+1 into the free
+  // slot (read by nobody still in step zo-1), barrier, read, refill phi
+  // plane zo+5 into zo-2's slot (no longer read by anyone past the barrier;
+  // first read three steps later).
+  int o_m2 = 0, o_m1 = C::FPL, o_0 = 2 * C::FPL, o_p1 = 3 * C::FPL, o_p2 = 4 * C::FPL, o_p3 = 5 * C::FPL,
+      o_p4 = 6 * C::FPL;
+  int n_m2 = 9 * C::NPL, n_m = 0, n_0 = 3 * C::NPL, n_f = 6 * C::NPL;
+  // phi refill sources: plane zo+5 of this thread's load slots, advanced per step
+  const float* pf[C::kPhiPer];
+#pragma unroll
+  for (int k = 0; k < C::kPhiPer; ++k) pf[k] = plane_ptr(z0 + 5) + phi_g[k];
   __syncthreads();
-  normal_plane_slow(n_m, z0 - 1);
-  normal_plane_slow(n_0, z0);
+  normal_plane_slow(Nr + n_m, z0 - 1);
+  normal_plane_slow(Nr + n_0, z0);
 
   const int z_stop = min(z0 + C::TZ, z_end);
   // static fields of the first output plane (then prefetched one plane ahead)
@@ -187,12 +193,13 @@ __global__ void __launch_bounds__(TX* TY, 2)
 #pragma unroll 1
     for (int t = 0; t < tend; ++t) {
       const int zo = zc + t;
-      // prefetch: phi plane zo+4 (ring refill) and the static fields at zo+1
+      // prefetch: phi plane zo+5 (ring refill) and the static fields at zo+1
       float nxt[C::kPhiPer];
-      {
-        const float* src = plane_ptr(zo + 4);
 #pragma unroll
-        for (int k = 0; k < C::kPhiPer; ++k) nxt[k] = phi_s[k] >= 0 ? __ldg(src + phi_g[k]) : 0.0f;
+      for (int k = 0; k < C::kPhiPer; ++k) nxt[k] = phi_s[k] >= 0 ? __ldg(pf[k]) : 0.0f;
+      if (zo + 6 <= g.ze - 1) {  // clamped at the last held plane
+#pragma unroll
+        for (int k = 0; k < C::kPhiPer; ++k) pf[k] += plane;
       }
       const float ki = ki_n, k1i = k1i_n;
       const size_t vo = vi;
@@ -204,19 +211,20 @@ __global__ void __launch_bounds__(TX* TY, 2)
 
       // normal plane zo+1 from phi planes (zo, zo+1, zo+2), face rule at z = nz-1
       if (zo + 2 <= nz - 1)
-        normal_plane(n_f, o_0, o_p1, o_p2, 0.5f);
+        normal_plane(Nr + n_f, o_0, o_p1, o_p2, 0.5f);
       else if (zo + 1 == nz - 1)
-        normal_plane(n_f, o_0, o_p1, o_p1, 1.0f);
+        normal_plane(Nr + n_f, o_0, o_p1, o_p1, 1.0f);
       else
-        normal_plane(n_f, o_m1, o_0, o_0, 1.0f);
+        normal_plane(Nr + n_f, o_m1, o_0, o_0, 1.0f);
       __syncthreads();
 
       {
         const int zmm = max(zo - 1, 0), zpp = min(zo + 1, nz - 1);
         const float invz = (zpp - zmm) == 2 ? 0.5f : 1.0f;
         // curvature kappa = div n (ops.cpp:281-316), same face rule
-        const float kappa = (n_0[n_xp] - n_0[n_xm]) * invx + (n_0[C::NPL + n_yp] - n_0[C::NPL + n_ym]) * invy +
-                            (n_f[2 * C::NPL + n_c] - n_m[2 * C::NPL + n_c]) * invz;
+        const float* N0 = Nr + n_0;
+        const float kappa = (N0[n_xp] - N0[n_xm]) * invx + (N0[C::NPL + n_yp] - N0[C::NPL + n_ym]) * invy +
+                            (Nr[n_f + 2 * C::NPL + n_c] - Nr[n_m + 2 * C::NPL + n_c]) * invz;
         // 7-point Laplacian, clamp-to-edge (ops.cpp:258-271)
         const float* pc = Phi + o_0 + s_c;
         const float cphi = pc[0];
@@ -255,20 +263,21 @@ __global__ void __launch_bounds__(TX* TY, 2)
         }
       }
       {
-        float* dst = Phi + o_m2;  // plane zo-2 is not read in this step: refill with zo+4
+        float* dst = Phi + o_m2;  // plane zo-2: no thread past this step's barrier reads it
 #pragma unroll
         for (int k = 0; k < C::kPhiPer; ++k)
           if (phi_s[k] >= 0) dst[phi_s[k]] = nxt[k];
       }
-      __syncthreads();
       const int ot = o_m2;
       o_m2 = o_m1;
       o_m1 = o_0;
       o_0 = o_p1;
       o_p1 = o_p2;
       o_p2 = o_p3;
-      o_p3 = ot;
-      float* nt = n_m;
+      o_p3 = o_p4;
+      o_p4 = ot;
+      const int nt = n_m2;
+      n_m2 = n_m;
       n_m = n_0;
       n_0 = n_f;
       n_f = nt;

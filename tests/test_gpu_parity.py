@@ -188,7 +188,7 @@ def test_tma_and_ldg_paths_bitwise(rsf, sigma1, fields, monkeypatch):
     img, phi, _ = case(40, 36, 32)
     p = _params(rsf, sigma1=sigma1, max_iters=3)
     a = rsf.evolve(phi, img, p, fields=fields)
-    monkeypatch.setenv("RSFG_NO_TMA", "1")
+    monkeypatch.setenv("RSFG_TMA", "1")
     b = rsf.evolve(phi, img, p, fields=fields)
     assert np.array_equal(a, b)
 
