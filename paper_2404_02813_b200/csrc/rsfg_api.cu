@@ -112,6 +112,7 @@ struct rsfg_slab {
   unsigned long long* h_counters = nullptr; // pinned mirror
   unsigned int* mm = nullptr;               // device min/max scratch
   rsfg::XYMaps xymaps[2] = {};              // TMA maps for kernel 1, per phi buffer
+  rsfg::ZMaps zmaps[2] = {};                // TMA maps for kernel 2 (zst4), per phi buffer
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -160,41 +161,73 @@ void release(rsfg_slab* s) {
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
-// TMA descriptors for kernel 1's tiles (3-D fp32 maps of the held planes).
-// Needs 16-byte row pitch (nx % 4 == 0); otherwise kernel 1 uses LDG.
-void make_xy_maps(rsfg_slab* s) {
-  s->xymaps[0].valid = s->xymaps[1].valid = false;
-  int bx = 0, by = 0;
-  // Opt-in: measured on B200 the single-shot TMA tile is not faster than the
-  // batched-LDG prologue at 512^3 (profiles/r01_tma_vs_ldg.txt); kept for the
-  // z-pipelined variant.
-  const char* on = std::getenv("RSFG_TMA");
-  if (!(on && on[0] == '1') || !s->fast || (s->nx % 4) != 0 || !rsfg::xy_tma_box(s->t1.r, &bx, &by)) return;
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
         q != cudaDriverEntryPointSuccess)
-      return;
+      return nullptr;
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  auto encode = [&](CUtensorMap* m, const float* ptr) {
-    const cuuint64_t dims[3] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny, (cuuint64_t)(s->ze - s->zb)};
-    const cuuint64_t strides[2] = {(cuuint64_t)s->nx * 4, (cuuint64_t)s->nx * s->ny * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
-    const cuuint32_t es[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  };
+  return enc;
+}
+
+// 3-D fp32 tensor map over the held planes of a slab buffer with `cols`
+// floats per row (nx, or 2*nx for float2 pairs) and the given box.
+bool encode_map(CUtensorMap* m, const void* ptr, int cols, int rows, int planes, int bx, int by, int bz) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)cols * 4, (cuuint64_t)cols * rows * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA descriptors for kernel 1's tiles (3-D fp32 maps of the held planes).
+// Needs 16-byte row pitch (nx % 4 == 0); otherwise kernel 1 uses LDG.
+void make_xy_maps(rsfg_slab* s) {
+  s->xymaps[0].valid = s->xymaps[1].valid = false;
+  int bx = 0, by = 0;
+  // Opt-in: measured on B200 the single-shot TMA tile is not faster than the
+  // batched-LDG prologue at 512^3 (profiles/r01_tma_vs_ldg.txt).
+  const char* on = std::getenv("RSFG_TMA");
+  if (!(on && on[0] == '1') || !s->fast || (s->nx % 4) != 0 || !rsfg::xy_tma_box(s->t1.r, &bx, &by)) return;
+  const int planes = s->ze - s->zb;
   CUtensorMap img;
-  if (!encode(&img, s->image)) return;
+  if (!encode_map(&img, s->image, s->nx, s->ny, planes, bx, by, 1)) return;
   for (int b = 0; b < 2; ++b) {
-    if (!encode(&s->xymaps[b].phi, s->phi[b])) return;
+    if (!encode_map(&s->xymaps[b].phi, s->phi[b], s->nx, s->ny, planes, bx, by, 1)) return;
     s->xymaps[b].img = img;
   }
   s->xymaps[0].valid = s->xymaps[1].valid = true;
+}
+
+// TMA descriptors for kernel 2 (zst4).  Needs nx % 4 == 0 (16-byte phi rows).
+// RSFG_ZST4=0 selects the LDG-staged kernel 2 instead.
+void make_z_maps(rsfg_slab* s) {
+  s->zmaps[0].valid = s->zmaps[1].valid = false;
+  const char* off = std::getenv("RSFG_ZST4");
+  if ((off && off[0] == '0') || !s->fast || (s->nx % 4) != 0) return;
+  int bz = 0;
+  if (!rsfg::zst4_box(s->t1.r, s->fields, &bz)) return;
+  const int planes = s->ze - s->zb;
+  // A P window deeper than the held planes is never loaded by TMA (the
+  // kernel's in-range test fails for every group); encode a valid map anyway.
+  rsfg::ZMaps m;
+  for (int f = 0; f < 2; ++f) {
+    const float2* P = s->P[f] ? s->P[f] : s->P[0];
+    if (!encode_map(&m.p[f], P, 2 * s->nx, s->ny, planes, 64, 8, std::min(bz, planes))) return;
+  }
+  for (int b = 0; b < 2; ++b) {
+    s->zmaps[b] = m;
+    if (!encode_map(&s->zmaps[b].phi, s->phi[b], s->nx, s->ny, planes, 40, 12, 1)) return;
+  }
+  s->zmaps[0].valid = s->zmaps[1].valid = true;
 }
 
 int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_params* p,
@@ -262,6 +295,7 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
   make_xy_maps(s);
+  make_z_maps(s);
   // Never-read halo planes must still be finite memory: zero everything once.
   CUDA_TRY(cudaMemsetAsync(s->phi[0], 0, held * sizeof(float), s->stream));
   CUDA_TRY(cudaMemsetAsync(s->phi[1], 0, held * sizeof(float), s->stream));
@@ -400,7 +434,10 @@ int step_finish(rsfg_slab* s, rsfg::StepMode mode, float* out) {
   rsfg::StepBuffers b = buffers(s, out);
   int n;
   if (s->fast) {
-    n = rsfg::launch_zst(g, s->fields, s->t1, s->c, b, s->z0, s->z1, mode, s->stream);
+    n = -1;
+    if (mode == rsfg::kUpdate)
+      n = rsfg::launch_zst4(g, s->fields, s->t1, s->c, b, s->z0, s->z1, s->zmaps[s->cur], s->stream);
+    if (n < 0) n = rsfg::launch_zst(g, s->fields, s->t1, s->c, b, s->z0, s->z1, mode, s->stream);
   } else {
     int m = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
                                       s->scratch, 0, 0, s->z0, s->z1, s->stream);

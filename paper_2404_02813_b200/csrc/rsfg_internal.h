@@ -63,6 +63,23 @@ struct XYMaps {
   bool valid;
 };
 
+// TMA descriptors of kernel 2's (zst4) inputs for one phi buffer: the phi
+// plane ring box (40 x 12 x 1 floats) and the P pair windows (P viewed as
+// 2*nx floats per row, box 64 x 8 x (8 + 2R)).  valid == false -> zst kernel.
+struct ZMaps {
+  CUtensorMap phi;
+  CUtensorMap p[2];
+  bool valid;
+};
+
+// Window depth (planes) of zst4's P box for radius r; false if zst4 has no
+// specialisation for (r, fields) or it does not fit shared memory.
+bool zst4_box(int r, int fields, int* pbox_z);
+
+// Kernel 2, TMA-fed variant (update mode only).  -1 when not applicable.
+int launch_zst4(const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b, int z_begin,
+                int z_end, const ZMaps& m, cudaStream_t st);
+
 // Box (x, y) of kernel 1's haloed input tile for radius r; false if no
 // specialised kernel exists.
 bool xy_tma_box(int r, int* bx, int* by);

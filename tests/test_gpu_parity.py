@@ -74,6 +74,38 @@ def test_ragged_shapes_P1(rsf, oracle, fields, shape):
     assert _rel_err(st.phi, ref_next) <= P1_TOL
 
 
+@pytest.mark.parametrize("fields", [2, 4])
+@pytest.mark.parametrize("shape", [(96, 28, 80), (132, 44, 70)])
+def test_interior_tiles_P1(rsf, oracle, fields, shape):
+    """Shapes with interior 32x8 tiles, several 64-plane CTAs in z and partial
+    8-plane groups: kernel 2's fast (constant-offset) and general variants."""
+    from _oracle import params
+    img, phi = random_case(*shape, seed=11)
+    op = params(sigma1=3.0)
+    ref_next, sc, _ = oracle.step(phi, img, op)
+    st = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0), fields=fields)
+    frac = st.step()
+    assert _rel_err(st.phi, ref_next) <= P1_TOL
+    assert abs(frac * phi.size - sc) <= max(2, 1e-4 * phi.size)
+
+
+@pytest.mark.parametrize("zst4", ["1", "0"])
+def test_kernel2_variants_P2(rsf, oracle, zst4, monkeypatch):
+    """Kernel 2 as the TMA-fed zst4 (default when nx % 4 == 0) and as the
+    LDG-staged zst (RSFG_ZST4=0): both within P2 of the oracle after 10 steps."""
+    from _oracle import params
+    monkeypatch.setenv("RSFG_ZST4", zst4)
+    img, phi, _ = case(96, 28, 80)
+    op = params(sigma1=3.0)
+    st_o = oracle.init(np.array(img), op)
+    ref = np.array(phi)
+    for _ in range(10):
+        ref, _, _ = oracle.step(ref, np.array(img), op, st_o)
+    st = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0))
+    st.run(10)
+    assert _rel_err(st.phi, ref) <= P2_TOL
+
+
 @pytest.mark.parametrize("sigma1", [7.0, 2.5])  # R=21 (generic path), R=8
 def test_generic_and_other_radii(rsf, oracle, sigma1):
     from _oracle import params

@@ -24,6 +24,21 @@ def test_slabs_bitwise(parts, fields):
     assert np.array_equal(ss.phi(), mono)
 
 
+@pytest.mark.parametrize("parts", [2, 3])
+def test_slabs_bitwise_interior_tiles(parts):
+    """Shape with interior tiles and several CTAs per slab (zst4 fast path)."""
+    import paper_2404_02813_b200 as rsf
+    from paper_2404_02813_b200.spmd import SlabSet
+    img, phi, _ = case(96, 28, 80)
+    p = rsf.RsfParams(sigma1=3.0)
+    st = rsf.init_evolution(phi, img, p)
+    ss = SlabSet(np.array(phi), np.array(img), p, parts)
+    for _ in range(4):
+        st.step()
+        ss.step()
+    assert np.array_equal(ss.phi(), st.phi)
+
+
 def test_slab_generic_radius_bitwise():
     import paper_2404_02813_b200 as rsf
     from paper_2404_02813_b200.spmd import SlabSet
