@@ -223,6 +223,8 @@ void make_z_maps(rsfg_slab* s) {
     const float2* P = s->P[f] ? s->P[f] : s->P[0];
     if (!encode_map(&m.p[f], P, 2 * s->nx, s->ny, planes, 64, 8, std::min(bz, planes))) return;
   }
+  if (!encode_map(&m.ki, s->ki, s->nx, s->ny, planes, 32, 8, 1)) return;
+  if (!encode_map(&m.k1i, s->k1i ? s->k1i : s->ki, s->nx, s->ny, planes, 32, 8, 1)) return;
   for (int b = 0; b < 2; ++b) {
     s->zmaps[b] = m;
     if (!encode_map(&s->zmaps[b].phi, s->phi[b], s->nx, s->ny, planes, 40, 12, 1)) return;

@@ -64,10 +64,11 @@ struct XYMaps {
 };
 
 // TMA descriptors of kernel 2's (zst4) inputs for one phi buffer: the phi
-// plane ring box (40 x 12 x 1 floats) and the P pair windows (P viewed as
+// plane ring box (40 x 12 x 1 floats), the static fields and the P pair windows (P viewed as
 // 2*nx floats per row, box 64 x 8 x (8 + 2R)).  valid == false -> zst kernel.
 struct ZMaps {
   CUtensorMap phi;
+  CUtensorMap ki, k1i;  // K2*I (== I for sigma2 = 0) and K1*I, box 32 x 8 x 1
   CUtensorMap p[2];
   bool valid;
 };

@@ -1,23 +1,29 @@
-// rsfg_zst4.cu -- kernel 2 of the RSF step, TMA-fed z-streaming variant:
+// rsfg_zst4.cuh -- kernel 2 of the RSF step, TMA-fed z-streaming variant:
 // z pass, region averages and force, curvature / Laplacian stencil, combine
 // and explicit update (reference rsf.cpp:96-168, 324-352; ops.cpp:109-160,
 // 199-316).  Same arithmetic as rsfg_zst.cu's kernel; what changes is how the
 // data reaches the threads:
 //
-//  * phi planes stream through an 8-slot shared ring filled by TMA (one
-//    elected thread, one mbarrier per slot, four planes of prefetch), so no
-//    thread spends instructions staging phi;
+//  * phi planes, and the static fields K2*I (== I when sigma2 = 0) and K1*I
+//    of the same plane, stream through an 8-slot shared ring filled by TMA
+//    (one elected thread, one mbarrier per slot, four planes of prefetch), so
+//    no thread spends instructions or registers staging them;
 //  * the z-pass input window (8 + 2R planes of the kernel-1 pairs P for the
 //    CTA's 32 x 8 columns) arrives as ONE 3-D TMA box per 8-plane group,
 //    issued a whole group ahead into a single buffer;
-//  * the plane loop is unrolled by 8 (the phi-ring period; the 4-slot normal
-//    ring divides it), so every ring access is a base register plus an
-//    immediate: no per-voxel address arithmetic;
+//  * the plane loop is unrolled by 8 (the ring period), so every shared
+//    access is a base register plus an immediate;
+//  * a thread keeps its own column's phi (planes q-1..q+2), the four in-plane
+//    phi neighbours of plane q and n_z (planes q-1..q+1) in registers: the
+//    shared normal ring holds only n_x, n_y of two planes, and one barrier per
+//    plane separates "normal of plane q+1" from "output of plane q", which run
+//    interleaved in the same step (independent work for the scheduler);
 //  * interior tiles away from the volume faces run a variant with constant
 //    neighbour offsets and the 1/2 central-difference factors folded into a
 //    doubled-gradient convention (n = 2g / max(|2g|, 2 floor) == g / max(|g|,
 //    floor) exactly); tiles or plane groups that touch a face run the general
-//    variant with per-thread clamped offsets and per-plane face factors.
+//    variant with clamped offsets and face factors (bitwise identical on
+//    interior voxels: the factors there are exact 1s).
 #pragma once
 #include <type_traits>
 
@@ -31,72 +37,42 @@ struct Z4 {
   static constexpr int TX = 32, TY = 8, NT = TX * TY;
   static constexpr int BX = 40, BY = 12, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
-  static constexpr int kHalo = NPL - NT;
-  static constexpr int G = 8;             // planes per group (z-pass chunk, ring period)
-  static constexpr int TZ = 64;           // planes per CTA
-  static constexpr int NW = G + 2 * R;    // z-pass window (planes)
-  static constexpr int PPL = TX * TY;     // float2 per P plane of the box
+  static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
+  static constexpr int G = 8;                             // planes per group (z-pass chunk, ring period)
+  static constexpr int TZ = 64;                           // planes per CTA
+  static constexpr int NW = G + 2 * R;                    // z-pass window (planes)
+  static constexpr int PPL = TX * TY;                     // float2 per P plane of the box
+  static constexpr int NK = NP == 1 ? 2 : 1;              // static fields per plane: K2*I (+ K1*I)
   static constexpr size_t kPBytes = (size_t)NP * NW * PPL * sizeof(float2);
   static constexpr size_t kPhiBytes = (size_t)8 * SLOT * sizeof(float);
-  static constexpr size_t kNrBytes = (size_t)4 * 3 * NPL * sizeof(float);
-  static constexpr size_t kSmem = kPBytes + kPhiBytes + kNrBytes + 16 * sizeof(uint64_t);
+  static constexpr size_t kKBytes = (size_t)8 * NK * NT * sizeof(float);
+  static constexpr size_t kNrBytes = (size_t)2 * 2 * NPL * sizeof(float);
+  static constexpr size_t kSmem = kPBytes + kPhiBytes + kKBytes + kNrBytes + 16 * sizeof(uint64_t);
+  static constexpr uint32_t kSlotTx = (uint32_t)((SLOT + NK * NT) * sizeof(float));
 };
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// One normal-plane position: phi-ring offset of its centre, neighbour deltas
-// and doubled-convention factors (1 central, 2 one-sided), normal-plane slot.
+// One normal-plane position: phi-ring offset of its centre, in-plane
+// neighbour deltas (clamped), doubled-convention factors (1 central, 2
+// one-sided) and its offset in a normal-plane slot.
 struct NPos {
   int s, dxm, dxp, dym, dyp, n;
   float fx, fy;
 };
 
-template <int R, int NP, bool GEN>
-struct Z4Body {
-  using C = Z4<R, NP>;
-
-  // n at one position of global plane q from ring slots (om, o0, op); fz =
-  // doubled-convention z factor.  dst = normal plane slot base.
-  static __device__ __forceinline__ void normal(const float* __restrict__ Phi, const NPos& p, int om, int o0,
-                                               int op, float fz, float inv2floor, float* __restrict__ dst) {
-    const float* c0 = Phi + o0 + p.s;
-    float a, bb, cc;
-    if constexpr (GEN) {
-      a = (c0[p.dxp] - c0[p.dxm]) * p.fx;
-      bb = (c0[p.dyp] - c0[p.dym]) * p.fy;
-      cc = (Phi[op + p.s] - Phi[om + p.s]) * fz;
-    } else {
-      a = c0[1] - c0[-1];
-      bb = c0[C::BX] - c0[-C::BX];
-      cc = Phi[op + p.s] - Phi[om + p.s];
-    }
-    const float inv = fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
-    float* d = dst + p.n;
-    d[0] = a * inv;
-    d[C::NPL] = bb * inv;
-    d[2 * C::NPL] = cc * inv;
-  }
-};
-
-template <int R, int NP>
-__global__ void __launch_bounds__(256, 2)
-    zst4_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end,
-                const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_p0,
-                const __grid_constant__ CUtensorMap map_p1);
-
-// --------------------------------------------------------------------------
-// The CTA program, templated on the xy variant (GX: general offsets).  The
-// z variant (faces, partial groups) is chosen per group at run time.
 template <int R, int NP, bool GX>
 __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const StepConsts& c, const StepBuffers& b,
                                          int z0, int z_stop, int x0, int y0, int bx0, int by0,
-                                         const CUtensorMap* map_phi, const CUtensorMap* map_p0,
+                                         const CUtensorMap* map_phi, const CUtensorMap* map_ki,
+                                         const CUtensorMap* map_k1i, const CUtensorMap* map_p0,
                                          const CUtensorMap* map_p1, unsigned char* smem, unsigned int& my_count) {
   using C = Z4<R, NP>;
-  float2* Pb = reinterpret_cast<float2*>(smem);                               // [NP][NW][TY][TX]
-  float* Phi = reinterpret_cast<float*>(smem + C::kPBytes);                   // [8][BY][BX]
-  float* Nr = Phi + 8 * C::SLOT;                                              // [4][3][NYr][NXr]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Nr + 4 * 3 * C::NPL);          // [8] phi slots, [8] P buffer
+  float2* Pb = reinterpret_cast<float2*>(smem);                       // [NP][NW][TY][TX]
+  float* Phi = reinterpret_cast<float*>(smem + C::kPBytes);           // [8][BY][BX]
+  float* Kr = Phi + 8 * C::SLOT;                                      // [8][NK][TY][TX]
+  float* Nr = Kr + 8 * C::NK * C::NT;                                 // [2][2][NYr][NXr]  (n_x, n_y)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Nr + 2 * 2 * C::NPL);  // [8] plane slots, [8] P buffer
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const long long plane = g.plane;
@@ -118,22 +94,23 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
     return p;
   };
   const NPos own = make_pos(tx + 1, ty + 1);
+  // halo: rows y0-1 and y0+TY (warps 0, 1), columns x0-1 and x0+TX (warp 2, lanes 0..15)
   const bool has_halo = tid < C::kHalo;
   NPos hal = own;
   if (has_halo) {
     int i, j;
-    if (tid < C::NXr) {
-      i = tid, j = 0;
-    } else if (tid < 2 * C::NXr) {
-      i = tid - C::NXr, j = C::NYr - 1;
+    if (tid < C::TX) {
+      i = tid + 1, j = 0;
+    } else if (tid < 2 * C::TX) {
+      i = tid - C::TX + 1, j = C::NYr - 1;
+    } else if (tid < 2 * C::TX + C::TY) {
+      i = 0, j = tid - 2 * C::TX + 1;
     } else {
-      const int k = tid - 2 * C::NXr;
-      i = (k & 1) ? C::NXr - 1 : 0;
-      j = 1 + (k >> 1);
+      i = C::NXr - 1, j = tid - 2 * C::TX - C::TY + 1;
     }
     hal = make_pos(i, j);
   }
-  // output voxel: kappa deltas in the normal plane and factors
+  // output voxel: kappa deltas in the normal plane, factors
   const int x = x0 + tx, y = y0 + ty;
   const bool col_ok = x < nx && y < ny;
   const int gxc = min(x, nx - 1), gyc = min(y, ny - 1);
@@ -143,12 +120,14 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   const float kfy = (kyp - kym) == 2 * C::NXr ? 1.0f : 2.0f;
   const size_t col = (size_t)gyc * nx + gxc;
 
-  // ---- TMA helpers (thread 0 only)
+  // ---- TMA producer (thread 0)
   auto zc_of = [&](int q) { return clampi(q, g.zb, g.ze - 1) - g.zb; };
-  auto issue_phi = [&](int q) {  // plane q -> slot (q - z0 + 2) & 7
+  auto issue_plane = [&](int q) {  // phi, K2*I (, K1*I) of plane q -> slot (q - z0 + 2) & 7
     const int sl = (q - z0 + 2) & 7;
-    mbar_expect_tx(bars + sl, (uint32_t)(C::SLOT * sizeof(float)));
+    mbar_expect_tx(bars + sl, C::kSlotTx);
     tma_load_3d(Phi + sl * C::SLOT, map_phi, bars + sl, bx0, by0, zc_of(q));
+    tma_load_3d(Kr + sl * C::NK * C::NT, map_ki, bars + sl, x0, y0, zc_of(q));
+    if (NP == 1) tma_load_3d(Kr + (sl * C::NK + 1) * C::NT, map_k1i, bars + sl, x0, y0, zc_of(q));
   };
   // P window of the group starting at zc: TMA when it lies inside the held
   // planes (no clamping needed), else threads load it with clamped LDG.
@@ -162,150 +141,158 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   if (tid == 0) {
     for (int i = 0; i < 9; ++i) mbar_init(bars + i, 1);
     const int last = min(z0 + 5, z_stop + 1);
-    for (int q = z0 - 2; q <= last; ++q) issue_phi(q);
+    for (int q = z0 - 2; q <= last; ++q) issue_plane(q);
     if (p_tma_ok(z0)) issue_p(z0);
   }
   __syncthreads();
 
-  // ---- prologue: normal planes z0-1 and z0 (normal slots 0 and 1)
-  for (int sl = 0; sl < 4; ++sl) mbar_wait(bars + sl, 0);
-  {
-    auto fzq = [&](int q) { return (q == 0 || q == nz - 1) ? 2.0f : 1.0f; };
-    // plane z0-1 from ring slots (0,1,2); plane z0 from (1,2,3)
-    Z4Body<R, NP, true>::normal(Phi, own, 0, C::SLOT, 2 * C::SLOT, fzq(z0 - 1), inv2floor, Nr);
-    if (has_halo) Z4Body<R, NP, true>::normal(Phi, hal, 0, C::SLOT, 2 * C::SLOT, fzq(z0 - 1), inv2floor, Nr);
-    Z4Body<R, NP, true>::normal(Phi, own, C::SLOT, 2 * C::SLOT, 3 * C::SLOT, fzq(z0), inv2floor, Nr + 3 * C::NPL);
-    if (has_halo)
-      Z4Body<R, NP, true>::normal(Phi, hal, C::SLOT, 2 * C::SLOT, 3 * C::SLOT, fzq(z0), inv2floor,
-                                  Nr + 3 * C::NPL);
-  }
+  // normal at a halo position of plane q (ring slots om, o0, op of q-1, q, q+1)
+  auto halo_normal = [&](auto genc, int om, int o0, int op, float fz, float* dst) {
+    constexpr bool GEN = decltype(genc)::value;
+    const float* c0 = Phi + o0 + hal.s;
+    float a, bb, cc;
+    if constexpr (GEN) {
+      a = (c0[hal.dxp] - c0[hal.dxm]) * hal.fx;
+      bb = (c0[hal.dyp] - c0[hal.dym]) * hal.fy;
+      cc = (Phi[op + hal.s] - Phi[om + hal.s]) * fz;
+    } else {
+      a = c0[1] - c0[-1];
+      bb = c0[C::BX] - c0[-C::BX];
+      cc = Phi[op + hal.s] - Phi[om + hal.s];
+    }
+    const float inv = fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
+    dst[hal.n] = a * inv;
+    dst[C::NPL + hal.n] = bb * inv;
+  };
+  auto fzq = [&](int q) { return (q == 0 || q == nz - 1) ? 2.0f : 1.0f; };
 
-  // ring base pointers (per thread), all accesses below add immediates
-  float* const Nown = Nr + own.n;
+  // ---- prologue: planes z0-2 .. z0+1 in slots 0..3
+  for (int sl = 0; sl < 4; ++sl) mbar_wait(bars + sl, 0);
+  const float* Pown = Phi + own.s;
+  float cm1 = Pown[1 * C::SLOT], c0 = Pown[2 * C::SLOT], cp1 = Pown[3 * C::SLOT];  // own phi z0-1, z0, z0+1
+  float nzm1, nz0;                                                                   // own n_z at z0-1, z0
+  float xm0, xp0, ym0, yp0;  // phi(z0) at the clamped in-plane neighbours
+  {
+    // n_z at (x, y, z0-1): needs the full gradient there
+    const float* p = Pown + 1 * C::SLOT;
+    const float a = (p[own.dxp] - p[own.dxm]) * own.fx, bb = (p[own.dyp] - p[own.dym]) * own.fy;
+    const float cc = (c0 - Pown[0]) * fzq(z0 - 1);
+    nzm1 = cc * fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
+  }
+  {
+    const float* p = Pown + 2 * C::SLOT;
+    xm0 = p[own.dxm], xp0 = p[own.dxp], ym0 = p[own.dym], yp0 = p[own.dyp];
+    const float a = (xp0 - xm0) * own.fx, bb = (yp0 - ym0) * own.fy, cc = (cp1 - cm1) * fzq(z0);
+    const float inv = fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
+    Nr[own.n] = a * inv;  // normal slot 0 <-> plane z0
+    Nr[C::NPL + own.n] = bb * inv;
+    nz0 = cc * inv;
+    if (has_halo) halo_normal(std::true_type{}, 1 * C::SLOT, 2 * C::SLOT, 3 * C::SLOT, fzq(z0), Nr);
+  }
 
   uint32_t pphase = 0;
-  float kib[8], k1ib[8];
-  // static-field prefetch two planes ahead (planes z0, z0+1)
-  {
-    const float* kip = b.ki + (size_t)(z0 - g.zb) * plane + col;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      kib[k] = (z0 + k < z_stop) ? __ldg(kip + (size_t)k * plane) : 0.0f;
-      if (NP == 1) k1ib[k] = (z0 + k < z_stop) ? __ldg(b.k1i + (size_t)(z0 + k - g.zb) * plane + col) : 0.0f;
-    }
-  }
-
 #pragma unroll 1
   for (int zc = z0, grp = 0; zc < z_stop; zc += C::G, ++grp) {
-    // ---- z pass for planes zc .. zc+7 (fp32 FMA per tap, ascending order,
-    // like the reference's f32-rounded z pass, ops.cpp:150-155)
+    // ---- z pass for planes zc .. zc+7 (fp32 FMA per tap, ascending tap
+    // order like the reference's f32-rounded z pass, ops.cpp:150-155),
+    // scattered from one window plane at a time into 8 accumulators.
     float2 kh[NP][C::G];
+    auto zpass = [&](auto load) {
+#pragma unroll
+      for (int np = 0; np < NP; ++np) {
+#pragma unroll
+        for (int kk = 0; kk < C::NW; ++kk) {
+          const float2 v = load(np, kk);
+#pragma unroll
+          for (int t = 0; t < C::G; ++t) {
+            const int j = kk - t;
+            if (j == 0) kh[np][t] = fmul2(taps.w[0], v);
+            else if (j > 0 && j <= 2 * R) kh[np][t] = ffma2(taps.w[j], v, kh[np][t]);
+          }
+        }
+      }
+    };
     if (p_tma_ok(zc)) {
       mbar_wait(bars + 8, pphase);
       pphase ^= 1;
-      const float2* src = Pb + ty * C::TX + tx;
-#pragma unroll
-      for (int np = 0; np < NP; ++np) {
-        float2 w[C::NW];
-#pragma unroll
-        for (int k = 0; k < C::NW; ++k) w[k] = src[(np * C::NW + k) * C::PPL];
-#pragma unroll
-        for (int t = 0; t < C::G; ++t) {
-          float2 acc = fmul2(taps.w[0], w[t]);
-#pragma unroll
-          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], w[t + j], acc);
-          kh[np][t] = acc;
-        }
-      }
+      const float2* src = Pb + tid;
+      zpass([&](int np, int kk) { return src[(np * C::NW + kk) * C::PPL]; });
     } else {
-#pragma unroll
-      for (int np = 0; np < NP; ++np) {
-        const float2* P = b.P[np] + col;
-        float2 w[C::NW];
-#pragma unroll
-        for (int k = 0; k < C::NW; ++k)
-          w[k] = __ldg(P + (size_t)(clampi(zc - R + k, g.zb, g.ze - 1) - g.zb) * (size_t)plane);
-#pragma unroll
-        for (int t = 0; t < C::G; ++t) {
-          float2 acc = fmul2(taps.w[0], w[t]);
-#pragma unroll
-          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], w[t + j], acc);
-          kh[np][t] = acc;
-        }
-      }
+      zpass([&](int np, int kk) {
+        return __ldg(b.P[np] + col + (size_t)(clampi(zc - R + kk, g.zb, g.ze - 1) - g.zb) * (size_t)plane);
+      });
     }
 
     const bool zfast = !GX && zc >= 1 && zc + C::G <= nz - 2 && zc + C::G <= z_stop;
     float* out = b.out + (size_t)(zc - g.zb) * plane + col;
-    const float* kip = b.ki + (size_t)(zc - g.zb) * plane + col;
-    const float* k1ip = b.k1i + (size_t)(zc - g.zb) * plane + col;
 
     auto step = [&](auto kc, auto genc) {
       constexpr int k = decltype(kc)::value;
       constexpr bool GEN = decltype(genc)::value;
-      using B = Z4Body<R, NP, GEN>;
-      const int zo = zc + k;
-      if (GEN && zo >= z_stop) return;  // partial last group (uniform)
-      // prefetch static fields two planes ahead
-      if (!GEN || zo + 2 < z_stop) {
-        kib[(k + 2) & 7] = __ldg(kip + (size_t)(k + 2) * plane);
-        if (NP == 1) k1ib[(k + 2) & 7] = __ldg(k1ip + (size_t)(k + 2) * plane);
-      }
-      // phi plane zo+2 (slot (k+4)&7) has landed?
-      mbar_wait(bars + ((k + 4) & 7), (uint32_t)((grp + (k >= 4 ? 1 : 0)) & 1));
-      // normal plane zo+1 into normal slot (k+2)&3 from phi slots of zo, zo+1, zo+2
-      {
-        constexpr int om = ((k + 2) & 7) * C::SLOT, o0 = ((k + 3) & 7) * C::SLOT, op = ((k + 4) & 7) * C::SLOT;
-        float* dst = Nr + ((k + 2) & 3) * 3 * C::NPL;
-        const float fz = GEN ? ((zo + 1 == 0 || zo + 1 == nz - 1) ? 2.0f : 1.0f) : 1.0f;
-        B::normal(Phi, own, om, o0, op, fz, inv2floor, dst);
-        if (has_halo) B::normal(Phi, hal, om, o0, op, fz, inv2floor, dst);
-      }
+      const int q = zc + k;
+      if (GEN && q >= z_stop) return;  // partial last group (uniform)
+      constexpr int o0 = ((k + 2) & 7) * C::SLOT, o1 = ((k + 3) & 7) * C::SLOT, o2 = ((k + 4) & 7) * C::SLOT;
+      constexpr int nq = (k & 1) * 2 * C::NPL, nq1 = ((k + 1) & 1) * 2 * C::NPL;
+      // normals of plane q (written in step q-1) complete; everybody is done
+      // with step q-1, so the ring slot of plane q-2 is free
       __syncthreads();
       if (tid == 0) {
-        // slot of plane zo-2 is free (last read in step zo-1): refill with zo+6
-        if (zo + 6 <= z_stop + 1) {
+        if (q + 6 <= z_stop + 1) {
           fence_proxy_async();
-          issue_phi(zo + 6);
+          issue_plane(q + 6);
         }
-        // the z pass of this group is done (all threads passed the barrier):
-        // prefetch the next group's P window into the single buffer
+        // the z pass of this group is done: next group's P window
         if (k == 0 && zc + C::G < z_stop && p_tma_ok(zc + C::G)) {
           fence_proxy_async();
           issue_p(zc + C::G);
         }
       }
-      // ---- output voxel (x, y, zo)
-      constexpr int s_m = ((k + 1) & 7) * C::SLOT, s_0 = ((k + 2) & 7) * C::SLOT, s_p = ((k + 3) & 7) * C::SLOT;
-      constexpr int n_m = ((k + 0) & 3) * 3 * C::NPL, n_0 = ((k + 1) & 3) * 3 * C::NPL,
-                    n_p = ((k + 2) & 3) * 3 * C::NPL;
-      const float* pc = Phi + s_0 + own.s;
-      const float cphi = pc[0];
-      float kappa, lap;
+      // plane q+2 (slot (k+4)&7) landed?  Issued for step q-4 / the prologue.
+      mbar_wait(bars + ((k + 4) & 7), (uint32_t)((grp + (k >= 4 ? 1 : 0)) & 1));
+
+      // ---- A: own normal at plane q+1 (n_x, n_y -> shared; n_z stays here)
+      const float* p1 = Pown + o1;
+      float xm1, xp1, ym1, yp1;
+      if constexpr (GEN) {
+        xm1 = p1[own.dxm], xp1 = p1[own.dxp], ym1 = p1[own.dym], yp1 = p1[own.dyp];
+      } else {
+        xm1 = p1[-1], xp1 = p1[1], ym1 = p1[-C::BX], yp1 = p1[C::BX];
+      }
+      const float cp2 = Pown[o2];
+      float a = xp1 - xm1, bb = yp1 - ym1, cc = cp2 - c0;
+      if constexpr (GEN) {
+        a *= own.fx;
+        bb *= own.fy;
+        cc *= fzq(q + 1);
+      }
+      const float inv = fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
+      Nr[nq1 + own.n] = a * inv;
+      Nr[nq1 + C::NPL + own.n] = bb * inv;
+      const float nzp1 = cc * inv;
+      if (has_halo) halo_normal(genc, o0, o1, o2, GEN ? fzq(q + 1) : 1.0f, Nr + nq1);
+
+      // ---- B: output voxel (x, y, q)
+      const float* N0 = Nr + nq + own.n;
+      float kappa;
       if constexpr (!GEN) {
         // kappa = div n (ops.cpp:281-316), doubled convention: 0.5 * sum of central differences
-        const float dx = Nown[n_0 + 1] - Nown[n_0 - 1];
-        const float dy = Nown[n_0 + C::NPL + C::NXr] - Nown[n_0 + C::NPL - C::NXr];
-        const float dz = Nown[n_p + 2 * C::NPL] - Nown[n_m + 2 * C::NPL];
-        kappa = 0.5f * ((dx + dy) + dz);
-        // 7-point Laplacian (ops.cpp:249-277)
-        lap = fmaf(-6.0f, cphi, ((pc[-1] + pc[1]) + (pc[-C::BX] + pc[C::BX])) + (Phi[s_m + own.s] + Phi[s_p + own.s]));
+        kappa = 0.5f * (((N0[1] - N0[-1]) + (N0[C::NPL + C::NXr] - N0[C::NPL - C::NXr])) + (nzp1 - nzm1));
       } else {
-        const float dx = (Nown[n_0 + kxp] - Nown[n_0 + kxm]) * kfx;
-        const float dy = (Nown[n_0 + C::NPL + kyp] - Nown[n_0 + C::NPL + kym]) * kfy;
-        // z face rule: zo == 0 -> n(1) - n(0); zo == nz-1 -> n(nz-1) - n(nz-2); factor 2
-        const int nzp = zo + 1 <= nz - 1 ? n_p : n_0;
-        const int nzm = zo - 1 >= 0 ? n_m : n_0;
-        const float fz = (zo + 1 <= nz - 1 && zo - 1 >= 0) ? 1.0f : 2.0f;
-        const float dz = (Nown[nzp + 2 * C::NPL] - Nown[nzm + 2 * C::NPL]) * fz;
-        kappa = 0.5f * ((dx + dy) + dz);
-        // clamped neighbours (the ring holds clamped planes in z)
-        lap = fmaf(-6.0f, cphi, ((pc[own.dxm] + pc[own.dxp]) + (pc[own.dym] + pc[own.dyp])) +
-                                    (Phi[s_m + own.s] + Phi[s_p + own.s]));
+        const float dx = (N0[kxp] - N0[kxm]) * kfx;
+        const float dy = (N0[C::NPL + kyp] - N0[C::NPL + kym]) * kfy;
+        // z face rule: q == 0 -> n(1) - n(0); q == nz-1 -> n(nz-1) - n(nz-2); factor 2
+        const float zp = q + 1 <= nz - 1 ? nzp1 : nz0;
+        const float zm = q - 1 >= 0 ? nzm1 : nz0;
+        const float fz = (q + 1 <= nz - 1 && q - 1 >= 0) ? 1.0f : 2.0f;
+        kappa = 0.5f * ((dx + dy) + (zp - zm) * fz);
       }
+      // 7-point Laplacian, clamp-to-edge (ops.cpp:249-277; the ring holds clamped planes)
+      const float lap = fmaf(-6.0f, c0, ((xm0 + xp0) + (ym0 + yp0)) + (cm1 + cp1));
       // delta_eps (rsf.cpp:96-107)
-      const float delta = c.c_delta * rcp_approx(fmaf(cphi, cphi, c.eps2));
+      const float delta = c.c_delta * rcp_approx(fmaf(c0, c0, c.eps2));
       // region averages r+- and F- - F+ (rsf.cpp:130-148, 164)
+      const float* K = Kr + ((k + 2) & 7) * C::NK * C::NT + tid;
+      const float ki = K[0];
       const float km = kh[0][k].x, kmi = kh[0][k].y;
       float kp, kpi;
       if constexpr (NP == 2) {
@@ -313,22 +300,28 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
         kpi = kh[NP - 1][k].y;
       } else {
         kp = 1.0f - km;
-        kpi = k1ib[k & 7] - kmi;
+        kpi = K[C::NT] - kmi;
       }
-      const float ki = kib[k & 7];
       // the floored denominators are >= denom_floor > FLT_MIN: plain rcp.approx
       const float rp = fminf(fmaxf(kpi * rcp_approx(fmaxf(kp, c.denom_floor)), c.i_min), c.i_max);
       const float rm = fminf(fmaxf(kmi * rcp_approx(fmaxf(km, c.denom_floor)), c.i_min), c.i_max);
       const float dF = (rp - rm) * (fmaf(2.0f, ki, -rp) - rm);
       // combine (rsf.cpp:151-168) and explicit update (rsf.cpp:340-344)
       const float e = (lap - kappa) + delta * fmaf(c.alpha, kappa, c.beta * dF);
-      const float f = fmaf(c.dt_f, e, cphi);
+      const float f = fmaf(c.dt_f, e, c0);
       if (col_ok) {
         out[(size_t)k * plane] = f;
-        my_count += ((cphi < 0.0f) != (f < 0.0f)) ? 1u : 0u;
+        my_count += ((c0 < 0.0f) != (f < 0.0f)) ? 1u : 0u;
         if (!(fabsf(f) <= 3.402823466e38f))
-          atomicMin(b.counters + 1, (unsigned long long)zo * (unsigned long long)plane + col);
+          atomicMin(b.counters + 1, (unsigned long long)q * (unsigned long long)plane + col);
       }
+      // ---- rotate the register windows to plane q+1
+      cm1 = c0;
+      c0 = cp1;
+      cp1 = cp2;
+      xm0 = xm1, xp0 = xp1, ym0 = ym1, yp0 = yp1;
+      nzm1 = nz0;
+      nz0 = nzp1;
     };
     using F = std::false_type;
     using T = std::true_type;
@@ -357,7 +350,8 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
 template <int R, int NP>
 __global__ void __launch_bounds__(256, 2)
     zst4_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end,
-                const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_p0,
+                const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_ki,
+                const __grid_constant__ CUtensorMap map_k1i, const __grid_constant__ CUtensorMap map_p0,
                 const __grid_constant__ CUtensorMap map_p1) {
   using C = Z4<R, NP>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -370,11 +364,11 @@ __global__ void __launch_bounds__(256, 2)
   unsigned int my_count = 0;
   const bool interior = x0 >= 2 && x0 + C::TX + 2 <= g.nx && y0 >= 2 && y0 + C::TY + 2 <= g.ny;
   if (interior)
-    zst4_cta<R, NP, false>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_p0, &map_p1, smem,
-                           my_count);
+    zst4_cta<R, NP, false>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
+                           &map_p1, smem, my_count);
   else
-    zst4_cta<R, NP, true>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_p0, &map_p1, smem,
-                          my_count);
+    zst4_cta<R, NP, true>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
+                          &map_p1, smem, my_count);
   const unsigned int wsum = __reduce_add_sync(0xffffffffu, my_count);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&s_count, wsum);
   __syncthreads();
@@ -395,7 +389,8 @@ int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuf
   }
   if (z_end <= z_begin) return 0;
   dim3 grid((z_end - z_begin + C::TZ - 1) / C::TZ, (g.nx + C::TX - 1) / C::TX, (g.ny + C::TY - 1) / C::TY);
-  k<<<grid, C::NT, C::kSmem, st>>>(g, t, c, b, z_begin, z_end, m.phi, m.p[0], NP == 2 ? m.p[1] : m.p[0]);
+  k<<<grid, C::NT, C::kSmem, st>>>(g, t, c, b, z_begin, z_end, m.phi, m.ki, NP == 1 ? m.k1i : m.ki, m.p[0],
+                                   NP == 2 ? m.p[1] : m.p[0]);
   return 1;
 }
 
