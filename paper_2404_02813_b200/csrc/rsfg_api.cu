@@ -113,6 +113,8 @@ struct rsfg_slab {
   unsigned int* mm = nullptr;               // device min/max scratch
   rsfg::XYMaps xymaps[2] = {};              // TMA maps for kernel 1, per phi buffer
   rsfg::ZMaps zmaps[2] = {};                // TMA maps for kernel 2 (zst4), per phi buffer
+  rsfg::XYMaps xy2maps[2] = {};             // TMA maps for kernel 1 (xy2), per phi buffer
+  int xy2_ty = 32;                          // xy2 tile height
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -207,6 +209,27 @@ void make_xy_maps(rsfg_slab* s) {
   s->xymaps[0].valid = s->xymaps[1].valid = true;
 }
 
+// TMA descriptors for kernel 1's multi-plane variant (xy2).  Needs nx % 4 ==
+// 0.  RSFG_XY2=0 selects the single-plane kernel 1; RSFG_XY2_TY=64 the
+// 64 x 64 tile.
+void make_xy2_maps(rsfg_slab* s) {
+  s->xy2maps[0].valid = s->xy2maps[1].valid = false;
+  const char* off = std::getenv("RSFG_XY2");
+  if ((off && off[0] == '0') || !s->fast || (s->nx % 4) != 0) return;
+  const char* ty = std::getenv("RSFG_XY2_TY");
+  s->xy2_ty = (ty && std::atoi(ty) == 64) ? 64 : 32;
+  int bx = 0, by = 0;
+  if (!rsfg::xy2_box(s->t1.r, s->xy2_ty, &bx, &by)) return;
+  const int planes = s->ze - s->zb;
+  CUtensorMap img;
+  if (!encode_map(&img, s->image, s->nx, s->ny, planes, bx, by, 1)) return;
+  for (int b = 0; b < 2; ++b) {
+    if (!encode_map(&s->xy2maps[b].phi, s->phi[b], s->nx, s->ny, planes, bx, by, 1)) return;
+    s->xy2maps[b].img = img;
+  }
+  s->xy2maps[0].valid = s->xy2maps[1].valid = true;
+}
+
 // TMA descriptors for kernel 2 (zst4).  Needs nx % 4 == 0 (16-byte phi rows).
 // RSFG_ZST4=0 selects the LDG-staged kernel 2 instead.
 void make_z_maps(rsfg_slab* s) {
@@ -298,6 +321,7 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
   make_xy_maps(s);
   make_z_maps(s);
+  make_xy2_maps(s);
   // Never-read halo planes must still be finite memory: zero everything once.
   CUDA_TRY(cudaMemsetAsync(s->phi[0], 0, held * sizeof(float), s->stream));
   CUDA_TRY(cudaMemsetAsync(s->phi[1], 0, held * sizeof(float), s->stream));
@@ -401,8 +425,11 @@ int xy_planes(rsfg_slab* s, int a, int b) {
   const rsfg::Geom g = s->geom();
   int n;
   if (s->fast) {
-    n = rsfg::launch_xy(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P[0], s->P[1], a, b,
-                        &s->xymaps[s->cur], s->stream);
+    n = rsfg::launch_xy2(g, s->fields, s->xy2_ty, s->t1, s->c.inv_eps, s->P[0], s->P[1], a, b, s->xy2maps[s->cur],
+                         s->stream);
+    if (n < 0)
+      n = rsfg::launch_xy(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P[0], s->P[1], a, b,
+                          &s->xymaps[s->cur], s->stream);
   } else {
     n = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
                                   s->scratch, a, b, 0, 0, s->stream);

@@ -85,6 +85,12 @@ int launch_zst4(const Geom& g, int fields, const Taps& t1, const StepConsts& c, 
 // specialised kernel exists.
 bool xy_tma_box(int r, int* bx, int* by);
 
+// Kernel 1, multi-plane TMA variant (xy2): tile 64 x ty (ty = 32 or 64).
+// xy2_box gives the raw-tile TMA box; launch_xy2 returns -1 when not applicable.
+bool xy2_box(int r, int ty, int* bx, int* by);
+int launch_xy2(const Geom& g, int fields, int ty, const Taps& t1, float inv_eps, float2* P0, float2* P1,
+               int z_begin, int z_end, const XYMaps& m, cudaStream_t st);
+
 // Kernel 1 ("xy"): Heaviside fields on a haloed tile + x pass + y pass ->
 // P for global planes [z_begin, z_end).  Returns the number of launches.
 int launch_xy(const Geom& g, int fields, const Taps& t1, float inv_eps, const float* phi,

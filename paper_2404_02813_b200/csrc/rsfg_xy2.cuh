@@ -1,0 +1,270 @@
+// rsfg_xy2.cuh -- kernel 1 of the RSF step, multi-plane TMA variant:
+// Heaviside fields of a haloed z-plane tile, then the x and y passes of the
+// separable Gaussian (reference rsf.cpp:75-94, ops.cpp:74-160).  Same
+// arithmetic and output (P pairs) as rsfg_xy.cu; what changes:
+//
+//  * a CTA owns one 64 x TY tile for NZC consecutive planes.  The raw phi and
+//    I tiles of plane z+1 are requested by TMA (one thread, one mbarrier) as
+//    soon as the Heaviside phase of plane z has consumed plane z's, so the
+//    load overlaps the x and y passes; no thread issues a global load;
+//  * the Heaviside fields of two adjacent voxels are evaluated with packed
+//    f32x2 arithmetic (FMUL2/FFMA2/FADD2: the atan polynomial runs once per
+//    pair), reading both voxels' phi and I with one 64-bit shared load each;
+//  * interior tiles (whole haloed window inside the volume) use constant
+//    offsets; edge tiles clamp every source index (clamp-to-edge,
+//    ops.cpp:48-70) and evaluate one voxel at a time.
+#pragma once
+#include "rsfg_device.cuh"
+
+namespace rsfg {
+namespace {
+
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; add.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mul.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 a,b,c,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mov.b64 c,{%6,%7}; fma.rn.f32x2 d,a,b,c; "
+      "mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
+
+// Heaviside pair of two voxels, packed: hm = H-(phi), hp = H+(phi) with
+// H+ = 1/2 [1 + (2/pi) atan(phi/eps)] (rsf.cpp:22-25, 89-90).  Same
+// evaluation as heaviside_pair (rsfg_device.cuh): atan(q)/pi on q = min(t,
+// 1/t) in [0, 1], and the small side of each pair is formed directly (never
+// as 1 - big) so both keep full relative precision.
+template <bool WANT_HP>
+__device__ __forceinline__ void heaviside2(float2 phi, float inv_eps, float2& hm, float2& hp) {
+  const float2 u = f2mul(phi, f2s(inv_eps));
+  const float tx = fabsf(u.x), ty = fabsf(u.y);
+  const float2 q = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
+  const float2 x = f2mul(q, q);
+  float2 p = f2fma(f2s(0.000906360219232738f), x, f2s(-0.00511184660717845f));
+  p = f2fma(p, x, f2s(0.013584661297500134f));
+  p = f2fma(p, x, f2s(-0.023883428424596786f));
+  p = f2fma(p, x, f2s(0.0338696613907814f));
+  p = f2fma(p, x, f2s(-0.04521126672625542f));
+  p = f2fma(p, x, f2s(0.06363844871520996f));
+  p = f2fma(p, x, f2s(-0.10610246658325195f));
+  p = f2fma(p, x, f2s(0.31830987334251404f));
+  const float2 a = f2mul(p, q);  // atan(q)/pi in [0, 1/4]
+  // sa = sign(u) * a.  near (t <= 1): H- = 1/2 - sa, H+ = 1/2 + sa.
+  // far (t > 1): H- = (u < 0) + sa, H+ = (u >= 0) - sa.
+  const float2 sa = make_float2(copysignf(a.x, u.x), copysignf(a.y, u.y));
+  const bool fx = tx > 1.0f, fy = ty > 1.0f;
+  const bool nx_ = u.x < 0.0f, ny_ = u.y < 0.0f;
+  const float2 m_near = f2add(f2s(0.5f), make_float2(-sa.x, -sa.y));
+  const float2 m_far = f2add(make_float2(nx_ ? 1.0f : 0.0f, ny_ ? 1.0f : 0.0f), sa);
+  hm = make_float2(fx ? m_far.x : m_near.x, fy ? m_far.y : m_near.y);
+  if constexpr (WANT_HP) {
+    const float2 p_near = f2add(f2s(0.5f), sa);
+    const float2 p_far = f2add(make_float2(nx_ ? 0.0f : 1.0f, ny_ ? 0.0f : 1.0f), make_float2(-sa.x, -sa.y));
+    hp = make_float2(fx ? p_far.x : p_near.x, fy ? p_far.y : p_near.y);
+  }
+}
+
+template <int R, int NP, int TY>
+struct XY2 {
+  static constexpr int TX = 64;
+  static constexpr int NT = TY >= 64 ? 512 : 256;
+  static constexpr int NZC = 8;  // planes per CTA
+  static constexpr int WX = TX + 2 * R, WY = TY + 2 * R;
+  // TMA box row: starts at (x0 - R) rounded down to 4 floats (16 bytes)
+  static constexpr int BOXX = (WX + 3 + 3) & ~3;
+  static constexpr int SHIFT = (64 * 1024 - R) & 3;  // (x0 - R) mod 4 for x0 % 64 == 0: interior tiles
+  static constexpr int PX = BOXX | 1;                // Hs pitch (float2), odd: conflict-free row-strided LDS.64
+  static constexpr int QX = TX | 1;
+  static constexpr int BX = 8, BY = 8;               // outputs per x-pass / y-pass item
+  static constexpr size_t kHsBytes = ((size_t)NP * WY * PX * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kXsBytes = ((size_t)NP * WY * QX * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kTile = ((size_t)BOXX * WY * sizeof(float) + 127) & ~(size_t)127;
+  static constexpr size_t kSmem = kHsBytes + kXsBytes + 2 * kTile + 16;
+  // interior Heaviside: pairs of raw columns [C0, C0 + 2*NPR) cover [SHIFT, SHIFT + WX)
+  static constexpr int C0 = SHIFT & ~1;
+  static constexpr int NPR = (SHIFT + WX - C0 + 1) / 2;
+};
+
+template <int R, int NP, int TY, bool EDGE>
+__device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float inv_eps, float2* __restrict__ P0,
+                                        float2* __restrict__ P1, int z_first, int z_last, int x0, int y0,
+                                        const CUtensorMap* map_phi, const CUtensorMap* map_img,
+                                        unsigned char* smem) {
+  using C = XY2<R, NP, TY>;
+  float2* Hs = reinterpret_cast<float2*>(smem);                                // [NP][WY][PX]
+  float2* Xs = reinterpret_cast<float2*>(smem + C::kHsBytes);                  // [NP][WY][QX]
+  float* Tphi = reinterpret_cast<float*>(smem + C::kHsBytes + C::kXsBytes);    // [WY][BOXX]
+  float* Timg = Tphi + C::kTile / sizeof(float);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kHsBytes + C::kXsBytes + 2 * C::kTile);
+  const int tid = threadIdx.x;
+  const int bx0 = max(x0 - R, 0) & ~3, by0 = max(y0 - R, 0);
+  // Hs column of window column ex: ex + xs (interior: the raw tile's column)
+  constexpr int xs = EDGE ? 0 : C::SHIFT;
+
+  auto issue = [&](int z) {
+    mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
+    tma_load_3d(Tphi, map_phi, bar, bx0, by0, z - g.zb);
+    tma_load_3d(Timg, map_img, bar, bx0, by0, z - g.zb);
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    issue(z_first);
+  }
+  __syncthreads();
+
+#pragma unroll 1
+  for (int z = z_first, ph = 0; z < z_last; ++z, ph ^= 1) {
+    mbar_wait(bar, (uint32_t)ph);
+    // ---- Phase A: Heaviside fields of the haloed tile -> Hs
+    if constexpr (!EDGE) {
+      // pairs of raw columns (c, c+1), c even: one LDS.64 of phi and of I each
+      constexpr int NPAIR = C::NPR * C::WY;
+#pragma unroll 2
+      for (int pi = tid; pi < NPAIR; pi += C::NT) {
+        const int ry = pi / C::NPR, c = C::C0 + 2 * (pi - ry * C::NPR);
+        const float2 pv = *reinterpret_cast<const float2*>(Tphi + ry * C::BOXX + c);
+        const float2 iv = *reinterpret_cast<const float2*>(Timg + ry * C::BOXX + c);
+        float2 hm, hp;
+        heaviside2<NP == 2>(pv, inv_eps, hm, hp);
+        const float2 hmi = f2mul(hm, iv);
+        float2* d = Hs + ry * C::PX + c;
+        d[0] = make_float2(hm.x, hmi.x);
+        d[1] = make_float2(hm.y, hmi.y);
+        if (NP == 2) {
+          const float2 hpi = f2mul(hp, iv);
+          d[C::WY * C::PX] = make_float2(hp.x, hpi.x);
+          d[C::WY * C::PX + 1] = make_float2(hp.y, hpi.y);
+        }
+      }
+    } else {
+      for (int e = tid; e < C::WX * C::WY; e += C::NT) {
+        const int ey = e / C::WX, ex = e - ey * C::WX;
+        const int cx = clampi(x0 - R + ex, 0, g.nx - 1) - bx0;
+        const int cy = clampi(y0 - R + ey, 0, g.ny - 1) - by0;
+        const float p = Tphi[cy * C::BOXX + cx], im = Timg[cy * C::BOXX + cx];
+        float hm, hp;
+        heaviside_pair(p, inv_eps, hm, hp);
+        Hs[ey * C::PX + ex] = make_float2(hm, hm * im);
+        if (NP == 2) Hs[C::WY * C::PX + ey * C::PX + ex] = make_float2(hp, hp * im);
+      }
+    }
+    __syncthreads();
+    // raw tiles consumed: fetch the next plane while the passes run
+    if (tid == 0 && z + 1 < z_last) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(z + 1);
+    }
+
+    // ---- Phase B: x pass, BX consecutive outputs per item; lanes walk rows
+    // so a half-warp reads 16 rows of the odd-pitched tile (no bank conflicts).
+    constexpr int SEGX = C::TX / C::BX;
+    for (int it = tid; it < NP * C::WY * SEGX; it += C::NT) {
+      const int np = it / (C::WY * SEGX);
+      const int rem = it - np * C::WY * SEGX;
+      const int sx = rem / C::WY, ry = rem - sx * C::WY;
+      const float2* src = Hs + np * C::WY * C::PX + ry * C::PX + xs + sx * C::BX;
+      float2 v[C::BX + 2 * R];
+#pragma unroll
+      for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
+      float2* dst = Xs + np * C::WY * C::QX + ry * C::QX + sx * C::BX;
+#pragma unroll
+      for (int b = 0; b < C::BX; ++b) {
+        float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+        for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+        dst[b] = acc;
+      }
+    }
+    __syncthreads();
+
+    // ---- Phase C: y pass, BY consecutive outputs down a column; lanes walk x.
+    constexpr int SEGY = TY / C::BY;
+    float2* Pz0 = P0 + (size_t)(z - g.zb) * (size_t)g.plane;
+    float2* Pz1 = NP == 2 ? P1 + (size_t)(z - g.zb) * (size_t)g.plane : nullptr;
+    for (int it = tid; it < NP * C::TX * SEGY; it += C::NT) {
+      const int np = it / (C::TX * SEGY);
+      const int rem = it - np * C::TX * SEGY;
+      const int sy = rem / C::TX, cx = rem - sy * C::TX;
+      const float2* src = Xs + np * C::WY * C::QX + (sy * C::BY) * C::QX + cx;
+      float2 v[C::BY + 2 * R];
+#pragma unroll
+      for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::QX];
+      const int gx = x0 + cx;
+      float2* Pz = np ? Pz1 : Pz0;
+#pragma unroll
+      for (int b = 0; b < C::BY; ++b) {
+        float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+        for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+        const int gy = y0 + sy * C::BY + b;
+        if (!EDGE || (gx < g.nx && gy < g.ny)) Pz[(size_t)gy * g.nx + gx] = acc;
+      }
+    }
+    // next plane's phase A rewrites Hs (last read in phase B, before the
+    // barrier above) and phase B rewrites Xs only after phase A's barrier,
+    // which every thread reaches after finishing this phase C.
+  }
+}
+
+template <int R, int NP, int TY>
+__global__ void __launch_bounds__(XY2<R, NP, TY>::NT, XY2<R, NP, TY>::NT == 256 ? 2 : 1)
+    xy2_kernel(Geom g, Taps taps, float inv_eps, float2* __restrict__ P0, float2* __restrict__ P1, int z_begin,
+               int z_end, const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_img) {
+  using C = XY2<R, NP, TY>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * TY;
+  const int z_first = z_begin + blockIdx.z * C::NZC;
+  const int z_last = min(z_first + C::NZC, z_end);
+  const bool edge = x0 - R < 0 || y0 - R < 0 || x0 - R + C::WX > g.nx || y0 - R + C::WY > g.ny;
+  if (edge)
+    xy2_cta<R, NP, TY, true>(g, taps, inv_eps, P0, P1, z_first, z_last, x0, y0, &map_phi, &map_img, smem);
+  else
+    xy2_cta<R, NP, TY, false>(g, taps, inv_eps, P0, P1, z_first, z_last, x0, y0, &map_phi, &map_img, smem);
+}
+
+template <int R, int NP, int TY>
+int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* P1, int z_begin, int z_end,
+               const XYMaps& m, cudaStream_t st) {
+  using C = XY2<R, NP, TY>;
+  if (C::kSmem > 227 * 1024) return -1;
+  auto k = xy2_kernel<R, NP, TY>;
+  static bool attr = false;  // benign race: idempotent attribute set
+  if (!attr) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  if (z_end <= z_begin) return 0;
+  dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
+  k<<<grid, C::NT, C::kSmem, st>>>(g, t, inv_eps, P0, P1, z_begin, z_end, m.phi, m.img);
+  return 1;
+}
+
+}  // namespace
+
+// kernel 1 tile height used by xy2 (RSFG_XY2_TY overrides: 32 or 64)
+constexpr int kXY2DefaultTY = 32;
+
+#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3)
+#define RSFG_XY2_DECL(N)                                                                                  \
+  int xy2_group_##N(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0,   \
+                    float2* P1, int z_begin, int z_end, const XYMaps& m, cudaStream_t st);                 \
+  int xy2_group_box_##N(int r, int ty, int* bx, int* by);
+RSFG_XY2_GROUPS(RSFG_XY2_DECL)
+#undef RSFG_XY2_DECL
+
+}  // namespace rsfg

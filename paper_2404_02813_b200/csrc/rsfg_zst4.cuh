@@ -38,8 +38,9 @@ struct Z4 {
   static constexpr int BX = 40, BY = 12, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
+  static constexpr int kProducer = 3 * 32;                // TMA-issuing thread (warp 3, no halo work)
   static constexpr int G = 8;                             // planes per group (z-pass chunk, ring period)
-  static constexpr int TZ = 64;                           // planes per CTA
+  static constexpr int TZ = 128;                          // planes per CTA
   static constexpr int NW = G + 2 * R;                    // z-pass window (planes)
   static constexpr int PPL = TX * TY;                     // float2 per P plane of the box
   static constexpr int NK = NP == 1 ? 2 : 1;              // static fields per plane: K2*I (+ K1*I)
@@ -94,7 +95,9 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
     return p;
   };
   const NPos own = make_pos(tx + 1, ty + 1);
-  // halo: rows y0-1 and y0+TY (warps 0, 1), columns x0-1 and x0+TX (warp 2, lanes 0..15)
+  // halo: rows y0-1 and y0+TY (warps 0, 1), columns x0-1 and x0+TX (warp 2,
+  // lanes 0..15); the TMA producer is warp 3 (kProducer), so no warp carries
+  // two of the extra jobs into the per-plane barrier.
   const bool has_halo = tid < C::kHalo;
   NPos hal = own;
   if (has_halo) {
@@ -120,7 +123,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   const float kfy = (kyp - kym) == 2 * C::NXr ? 1.0f : 2.0f;
   const size_t col = (size_t)gyc * nx + gxc;
 
-  // ---- TMA producer (thread 0)
+  // ---- TMA producer (thread kProducer)
   auto zc_of = [&](int q) { return clampi(q, g.zb, g.ze - 1) - g.zb; };
   auto issue_plane = [&](int q) {  // phi, K2*I (, K1*I) of plane q -> slot (q - z0 + 2) & 7
     const int sl = (q - z0 + 2) & 7;
@@ -138,7 +141,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
     if (NP == 2) tma_load_3d(Pb + C::NW * C::PPL, map_p1, bars + 8, 2 * x0, y0, zc - R - g.zb);
   };
 
-  if (tid == 0) {
+  if (tid == C::kProducer) {
     for (int i = 0; i < 9; ++i) mbar_init(bars + i, 1);
     const int last = min(z0 + 5, z_stop + 1);
     for (int q = z0 - 2; q <= last; ++q) issue_plane(q);
@@ -236,7 +239,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       // normals of plane q (written in step q-1) complete; everybody is done
       // with step q-1, so the ring slot of plane q-2 is free
       __syncthreads();
-      if (tid == 0) {
+      if (tid == C::kProducer) {
         if (q + 6 <= z_stop + 1) {
           fence_proxy_async();
           issue_plane(q + 6);
