@@ -10,9 +10,10 @@
 //  * the Heaviside fields of two adjacent voxels are evaluated with packed
 //    f32x2 arithmetic (FMUL2/FFMA2/FADD2: the atan polynomial runs once per
 //    pair), reading both voxels' phi and I with one 64-bit shared load each;
-//  * interior tiles (whole haloed window inside the volume) use constant
-//    offsets; edge tiles clamp every source index (clamp-to-edge,
-//    ops.cpp:48-70) and evaluate one voxel at a time.
+//  * every tile loads the same box layout (origin (x0 - R) rounded down to
+//    16 bytes, possibly negative); edge tiles first overwrite the positions
+//    outside the volume with their clamp-to-edge values, then all tiles run
+//    the same paired path.
 #pragma once
 #include "rsfg_device.cuh"
 
@@ -111,9 +112,12 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
   float* Timg = Tphi + C::kTile / sizeof(float);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kHsBytes + C::kXsBytes + 2 * C::kTile);
   const int tid = threadIdx.x;
-  const int bx0 = max(x0 - R, 0) & ~3, by0 = max(y0 - R, 0);
-  // Hs column of window column ex: ex + xs (interior: the raw tile's column)
-  constexpr int xs = EDGE ? 0 : C::SHIFT;
+  // Box origin: (x0 - R) rounded down to 16 bytes, y0 - R.  Starts may be
+  // negative (TMA zero-fills outside the volume; only a non-16-byte-aligned x
+  // start faults, tools/microbench/tma_neg.cu); edge tiles then overwrite the
+  // outside positions with their clamp-to-edge values (ops.cpp:48-70) so
+  // every tile runs the same paired Heaviside path.
+  const int bx0 = x0 - R - C::SHIFT, by0 = y0 - R;
 
   auto issue = [&](int z) {
     mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
@@ -129,9 +133,33 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
 #pragma unroll 1
   for (int z = z_first, ph = 0; z < z_last; ++z, ph ^= 1) {
     mbar_wait(bar, (uint32_t)ph);
-    // ---- Phase A: Heaviside fields of the haloed tile -> Hs
-    if constexpr (!EDGE) {
-      // pairs of raw columns (c, c+1), c even: one LDS.64 of phi and of I each
+    if constexpr (EDGE) {
+      // raw columns [0, lo) lie left of x = 0, [hi, BOXX) right of nx - 1
+      const int lo = max(0, -bx0), hi = min(C::BOXX, g.nx - bx0);
+      const int nfix = lo + (C::BOXX - hi);
+      for (int e = tid; e < C::WY * nfix; e += C::NT) {
+        const int ry = e / nfix, k = e - ry * nfix;
+        const int cdst = k < lo ? k : hi + (k - lo);
+        const int csrc = k < lo ? lo : hi - 1;
+        Tphi[ry * C::BOXX + cdst] = Tphi[ry * C::BOXX + csrc];
+        Timg[ry * C::BOXX + cdst] = Timg[ry * C::BOXX + csrc];
+      }
+      __syncthreads();
+      // rows [0, ylo) above y = 0, [yhi, WY) below ny - 1 (whole rows, after the column fix)
+      const int ylo = max(0, -by0), yhi = min(C::WY, g.ny - by0);
+      const int nrow = ylo + (C::WY - yhi);
+      for (int e = tid; e < nrow * C::BOXX; e += C::NT) {
+        const int k = e / C::BOXX, cx = e - k * C::BOXX;
+        const int rdst = k < ylo ? k : yhi + (k - ylo);
+        const int rsrc = k < ylo ? ylo : yhi - 1;
+        Tphi[rdst * C::BOXX + cx] = Tphi[rsrc * C::BOXX + cx];
+        Timg[rdst * C::BOXX + cx] = Timg[rsrc * C::BOXX + cx];
+      }
+      __syncthreads();
+    }
+    // ---- Phase A: Heaviside fields of the haloed tile -> Hs.  Pairs of raw
+    // columns (c, c+1), c even: one LDS.64 of phi and of I each.
+    {
       constexpr int NPAIR = C::NPR * C::WY;
 #pragma unroll 2
       for (int pi = tid; pi < NPAIR; pi += C::NT) {
@@ -150,17 +178,6 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
           d[C::WY * C::PX + 1] = make_float2(hp.y, hpi.y);
         }
       }
-    } else {
-      for (int e = tid; e < C::WX * C::WY; e += C::NT) {
-        const int ey = e / C::WX, ex = e - ey * C::WX;
-        const int cx = clampi(x0 - R + ex, 0, g.nx - 1) - bx0;
-        const int cy = clampi(y0 - R + ey, 0, g.ny - 1) - by0;
-        const float p = Tphi[cy * C::BOXX + cx], im = Timg[cy * C::BOXX + cx];
-        float hm, hp;
-        heaviside_pair(p, inv_eps, hm, hp);
-        Hs[ey * C::PX + ex] = make_float2(hm, hm * im);
-        if (NP == 2) Hs[C::WY * C::PX + ey * C::PX + ex] = make_float2(hp, hp * im);
-      }
     }
     __syncthreads();
     // raw tiles consumed: fetch the next plane while the passes run
@@ -176,7 +193,7 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
       const int np = it / (C::WY * SEGX);
       const int rem = it - np * C::WY * SEGX;
       const int sx = rem / C::WY, ry = rem - sx * C::WY;
-      const float2* src = Hs + np * C::WY * C::PX + ry * C::PX + xs + sx * C::BX;
+      const float2* src = Hs + np * C::WY * C::PX + ry * C::PX + C::SHIFT + sx * C::BX;
       float2 v[C::BX + 2 * R];
 #pragma unroll
       for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
