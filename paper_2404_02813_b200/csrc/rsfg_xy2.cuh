@@ -98,6 +98,10 @@ struct XY2 {
   // interior Heaviside: pairs of raw columns [C0, C0 + 2*NPR) cover [SHIFT, SHIFT + WX)
   static constexpr int C0 = SHIFT & ~1;
   static constexpr int NPR = (SHIFT + WX - C0 + 1) / 2;
+  static constexpr int RG = NT / NPR;                     // row groups of phase A
+  static constexpr int RITER = (WY + RG - 1) / RG;        // rows per phase-A thread
+  static constexpr int XIT = (NP * WY * (TX / BX) + NT - 1) / NT;  // x-pass items per thread
+  static constexpr int YIT = (NP * TX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
 };
 
 template <int R, int NP, int TY, bool EDGE>
@@ -118,6 +122,45 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
   // outside positions with their clamp-to-edge values (ops.cpp:48-70) so
   // every tile runs the same paired Heaviside path.
   const int bx0 = x0 - R - C::SHIFT, by0 = y0 - R;
+
+  // ---- per-thread work descriptors (constant across the CTA's planes)
+  // phase A: pair column pc of row group rg
+  const int a_pc = tid % C::NPR, a_rg = tid / C::NPR;
+  const bool a_on = a_rg < C::RG;
+  const bool a_last = a_rg + (C::RITER - 1) * C::RG < C::WY;
+  const float* Ta = Tphi + a_rg * C::BOXX + C::C0 + 2 * a_pc;
+  float2* Ha = Hs + a_rg * C::PX + C::C0 + 2 * a_pc;
+  // phase B items tid + i*NT -> (np, sx, ry)
+  int xsrc[C::XIT], xdst[C::XIT];
+  constexpr int SEGX = C::TX / C::BX;
+#pragma unroll
+  for (int i = 0; i < C::XIT; ++i) {
+    const int it = min(tid + i * C::NT, NP * C::WY * SEGX - 1);
+    const int np = it / (C::WY * SEGX);
+    const int rem = it - np * C::WY * SEGX;
+    const int sx = rem / C::WY, ry = rem - sx * C::WY;
+    xsrc[i] = np * C::WY * C::PX + ry * C::PX + C::SHIFT + sx * C::BX;
+    xdst[i] = np * C::WY * C::QX + ry * C::QX + sx * C::BX;
+  }
+  const bool x_last = tid + (C::XIT - 1) * C::NT < NP * C::WY * SEGX;
+  // phase C items tid + i*NT -> (np, sy, cx)
+  int ysrc[C::YIT], ygx[C::YIT], ygy[C::YIT];
+  bool ynp[C::YIT];
+  size_t yout[C::YIT];
+  constexpr int SEGY = TY / C::BY;
+#pragma unroll
+  for (int i = 0; i < C::YIT; ++i) {
+    const int it = min(tid + i * C::NT, NP * C::TX * SEGY - 1);
+    const int np = it / (C::TX * SEGY);
+    const int rem = it - np * C::TX * SEGY;
+    const int sy = rem / C::TX, cx = rem - sy * C::TX;
+    ysrc[i] = np * C::WY * C::QX + (sy * C::BY) * C::QX + cx;
+    ynp[i] = np != 0;
+    ygx[i] = x0 + cx;
+    ygy[i] = y0 + sy * C::BY;
+    yout[i] = (size_t)min(ygy[i], g.ny - 1) * g.nx + min(ygx[i], g.nx - 1);
+  }
+  const bool y_last = tid + (C::YIT - 1) * C::NT < NP * C::TX * SEGY;
 
   auto issue = [&](int z) {
     mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
@@ -158,24 +201,26 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
       __syncthreads();
     }
     // ---- Phase A: Heaviside fields of the haloed tile -> Hs.  Pairs of raw
-    // columns (c, c+1), c even: one LDS.64 of phi and of I each.
-    {
-      constexpr int NPAIR = C::NPR * C::WY;
-#pragma unroll 2
-      for (int pi = tid; pi < NPAIR; pi += C::NT) {
-        const int ry = pi / C::NPR, c = C::C0 + 2 * (pi - ry * C::NPR);
-        const float2 pv = *reinterpret_cast<const float2*>(Tphi + ry * C::BOXX + c);
-        const float2 iv = *reinterpret_cast<const float2*>(Timg + ry * C::BOXX + c);
-        float2 hm, hp;
-        heaviside2<NP == 2>(pv, inv_eps, hm, hp);
-        const float2 hmi = f2mul(hm, iv);
-        float2* d = Hs + ry * C::PX + c;
-        d[0] = make_float2(hm.x, hmi.x);
-        d[1] = make_float2(hm.y, hmi.y);
-        if (NP == 2) {
-          const float2 hpi = f2mul(hp, iv);
-          d[C::WY * C::PX] = make_float2(hp.x, hpi.x);
-          d[C::WY * C::PX + 1] = make_float2(hp.y, hpi.y);
+    // columns (c, c+1), c even: one LDS.64 of phi and of I each.  Thread
+    // (rg, pc) owns pair column pc of rows rg, rg + RG, ... (constant offsets).
+    if (a_on) {
+#pragma unroll
+      for (int i = 0; i < C::RITER; ++i) {
+        if (i < C::RITER - 1 || a_last) {
+          const int ro = i * C::RG;
+          const float2 pv = *reinterpret_cast<const float2*>(Ta + ro * C::BOXX);
+          const float2 iv = *reinterpret_cast<const float2*>(Ta + C::kTile / sizeof(float) + ro * C::BOXX);
+          float2 hm, hp;
+          heaviside2<NP == 2>(pv, inv_eps, hm, hp);
+          const float2 hmi = f2mul(hm, iv);
+          float2* d = Ha + ro * C::PX;
+          d[0] = make_float2(hm.x, hmi.x);
+          d[1] = make_float2(hm.y, hmi.y);
+          if (NP == 2) {
+            const float2 hpi = f2mul(hp, iv);
+            d[C::WY * C::PX] = make_float2(hp.x, hpi.x);
+            d[C::WY * C::PX + 1] = make_float2(hp.y, hpi.y);
+          }
         }
       }
     }
@@ -188,47 +233,46 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
 
     // ---- Phase B: x pass, BX consecutive outputs per item; lanes walk rows
     // so a half-warp reads 16 rows of the odd-pitched tile (no bank conflicts).
-    constexpr int SEGX = C::TX / C::BX;
-    for (int it = tid; it < NP * C::WY * SEGX; it += C::NT) {
-      const int np = it / (C::WY * SEGX);
-      const int rem = it - np * C::WY * SEGX;
-      const int sx = rem / C::WY, ry = rem - sx * C::WY;
-      const float2* src = Hs + np * C::WY * C::PX + ry * C::PX + C::SHIFT + sx * C::BX;
-      float2 v[C::BX + 2 * R];
 #pragma unroll
-      for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
-      float2* dst = Xs + np * C::WY * C::QX + ry * C::QX + sx * C::BX;
+    for (int i = 0; i < C::XIT; ++i) {
+      if (i < C::XIT - 1 || x_last) {
+        const float2* src = Hs + xsrc[i];
+        float2 v[C::BX + 2 * R];
 #pragma unroll
-      for (int b = 0; b < C::BX; ++b) {
-        float2 acc = fmul2(taps.w[0], v[b]);
+        for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
+        float2* dst = Xs + xdst[i];
 #pragma unroll
-        for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-        dst[b] = acc;
+        for (int b = 0; b < C::BX; ++b) {
+          float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+          dst[b] = acc;
+        }
       }
     }
     __syncthreads();
 
     // ---- Phase C: y pass, BY consecutive outputs down a column; lanes walk x.
-    constexpr int SEGY = TY / C::BY;
-    float2* Pz0 = P0 + (size_t)(z - g.zb) * (size_t)g.plane;
-    float2* Pz1 = NP == 2 ? P1 + (size_t)(z - g.zb) * (size_t)g.plane : nullptr;
-    for (int it = tid; it < NP * C::TX * SEGY; it += C::NT) {
-      const int np = it / (C::TX * SEGY);
-      const int rem = it - np * C::TX * SEGY;
-      const int sy = rem / C::TX, cx = rem - sy * C::TX;
-      const float2* src = Xs + np * C::WY * C::QX + (sy * C::BY) * C::QX + cx;
-      float2 v[C::BY + 2 * R];
+    {
+      float2* Pz0 = P0 + (size_t)(z - g.zb) * (size_t)g.plane;
+      float2* Pz1 = NP == 2 ? P1 + (size_t)(z - g.zb) * (size_t)g.plane : nullptr;
 #pragma unroll
-      for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::QX];
-      const int gx = x0 + cx;
-      float2* Pz = np ? Pz1 : Pz0;
+      for (int i = 0; i < C::YIT; ++i) {
+        if (i < C::YIT - 1 || y_last) {
+          const float2* src = Xs + ysrc[i];
+          float2 v[C::BY + 2 * R];
 #pragma unroll
-      for (int b = 0; b < C::BY; ++b) {
-        float2 acc = fmul2(taps.w[0], v[b]);
+          for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::QX];
+          float2* Pz = (NP == 2 && ynp[i]) ? Pz1 : Pz0;
+          float2* out = Pz + yout[i];
 #pragma unroll
-        for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-        const int gy = y0 + sy * C::BY + b;
-        if (!EDGE || (gx < g.nx && gy < g.ny)) Pz[(size_t)gy * g.nx + gx] = acc;
+          for (int b = 0; b < C::BY; ++b) {
+            float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+            for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+            if (!EDGE || (ygx[i] < g.nx && ygy[i] + b < g.ny)) out[(size_t)b * g.nx] = acc;
+          }
+        }
       }
     }
     // next plane's phase A rewrites Hs (last read in phase B, before the
