@@ -39,6 +39,7 @@ struct Z4 {
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
   static constexpr int kProducer = 3 * 32;                // TMA-issuing thread (warp 3, no halo work)
+  static_assert(kHalo > 2 * 32 && kHalo <= 2 * 32 + 16, "halo slots: warps 0, 1 and half of warp 2");
   static constexpr int G = 8;                             // planes per group (z-pass chunk, ring period)
   static constexpr int TZ = 128;                          // planes per CTA
   static constexpr int NW = G + 2 * R;                    // z-pass window (planes)
@@ -74,10 +75,12 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   float* Kr = Phi + 8 * C::SLOT;                                      // [8][NK][TY][TX]
   float* Nr = Kr + 8 * C::NK * C::NT;                                 // [2][2][NYr][NXr]  (n_x, n_y)
   uint64_t* bars = reinterpret_cast<uint64_t*>(Nr + 2 * 2 * C::NPL);  // [8] plane slots, [8] P buffer
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, lane = tid & 31;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const long long plane = g.plane;
   const float inv2floor = 0.5f * c.inv_grad_floor;
+  const bool producer_warp = __any_sync(0xffffffffu, tid == C::kProducer);  // warp-uniform
+  bool any_bad = false;  // a non-finite phi' in this thread's outputs (rare; rescanned at the end)
 
   // ---- positions.  Ring offset of global (gx, gy): (gy - by0) * BX + (gx - bx0).
   auto make_pos = [&](int i, int j) {  // normal-plane position (i, j) <-> global (x0-1+i, y0-1+j)
@@ -98,18 +101,22 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   // halo: rows y0-1 and y0+TY (warps 0, 1), columns x0-1 and x0+TX (warp 2,
   // lanes 0..15); the TMA producer is warp 3 (kProducer), so no warp carries
   // two of the extra jobs into the per-plane barrier.
-  const bool has_halo = tid < C::kHalo;
+  // Warps 0..2 all take the halo branch (warp-uniform: no reconvergence
+  // bookkeeping); warp 2's lanes 16..31 repeat lanes 0..15 (same values to the
+  // same addresses).
+  const bool has_halo = __any_sync(0xffffffffu, tid < C::kHalo);
   NPos hal = own;
   if (has_halo) {
     int i, j;
-    if (tid < C::TX) {
-      i = tid + 1, j = 0;
-    } else if (tid < 2 * C::TX) {
-      i = tid - C::TX + 1, j = C::NYr - 1;
-    } else if (tid < 2 * C::TX + C::TY) {
-      i = 0, j = tid - 2 * C::TX + 1;
+    const int h = tid < C::kHalo ? tid : tid - 16;
+    if (h < C::TX) {
+      i = h + 1, j = 0;
+    } else if (h < 2 * C::TX) {
+      i = h - C::TX + 1, j = C::NYr - 1;
+    } else if (h < 2 * C::TX + C::TY) {
+      i = 0, j = h - 2 * C::TX + 1;
     } else {
-      i = C::NXr - 1, j = tid - 2 * C::TX - C::TY + 1;
+      i = C::NXr - 1, j = h - 2 * C::TX - C::TY + 1;
     }
     hal = make_pos(i, j);
   }
@@ -239,7 +246,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       // normals of plane q (written in step q-1) complete; everybody is done
       // with step q-1, so the ring slot of plane q-2 is free
       __syncthreads();
-      if (tid == C::kProducer) {
+      if (producer_warp && lane == 0) {
         if (q + 6 <= z_stop + 1) {
           fence_proxy_async();
           issue_plane(q + 6);
@@ -312,11 +319,10 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       // combine (rsf.cpp:151-168) and explicit update (rsf.cpp:340-344)
       const float e = (lap - kappa) + delta * fmaf(c.alpha, kappa, c.beta * dF);
       const float f = fmaf(c.dt_f, e, c0);
-      if (col_ok) {
+      if (!GX || col_ok) {
         out[(size_t)k * plane] = f;
         my_count += ((c0 < 0.0f) != (f < 0.0f)) ? 1u : 0u;
-        if (!(fabsf(f) <= 3.402823466e38f))
-          atomicMin(b.counters + 1, (unsigned long long)q * (unsigned long long)plane + col);
+        any_bad |= !(fabsf(f) <= 3.402823466e38f);
       }
       // ---- rotate the register windows to plane q+1
       cm1 = c0;
@@ -346,6 +352,18 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       step(std::integral_constant<int, 5>{}, T{});
       step(std::integral_constant<int, 6>{}, T{});
       step(std::integral_constant<int, 7>{}, T{});
+    }
+  }
+  // Rare path (evolve_step's blowup report, rsf.cpp:324-352): some thread saw a
+  // non-finite phi'.  Rescan this thread's column of the CTA's planes for the
+  // first one (the CTA's own stores, visible to the thread that made them).
+  if (__any_sync(0xffffffffu, any_bad) && any_bad) {
+    for (int q = z0; q < z_stop; ++q) {
+      const float f = b.out[(size_t)(q - g.zb) * plane + col];
+      if (!(fabsf(f) <= 3.402823466e38f)) {
+        atomicMin(b.counters + 1, (unsigned long long)q * (unsigned long long)plane + col);
+        break;
+      }
     }
   }
 }
