@@ -3,6 +3,9 @@
 // separable Gaussian (reference rsf.cpp:75-94, ops.cpp:74-160).  Same
 // arithmetic and output (P pairs) as rsfg_xy.cu; what changes:
 //
+//  * the y pass runs first (it carries the x halo: WX/TX = 1.28 < WY/TY =
+//    1.56 at R = 9), then the x pass writes a staging tile that leaves as
+//    coalesced 16-byte stores;
 //  * a CTA owns one 64 x TY tile for NZC consecutive planes.  The raw phi and
 //    I tiles of plane z+1 are requested by TMA (one thread, one mbarrier) as
 //    soon as the Heaviside phase of plane z has consumed plane z's, so the
@@ -87,21 +90,34 @@ struct XY2 {
   static constexpr int WX = TX + 2 * R, WY = TY + 2 * R;
   // TMA box row: starts at (x0 - R) rounded down to 4 floats (16 bytes)
   static constexpr int BOXX = (WX + 3 + 3) & ~3;
-  static constexpr int SHIFT = (64 * 1024 - R) & 3;  // (x0 - R) mod 4 for x0 % 64 == 0: interior tiles
-  static constexpr int PX = BOXX | 1;                // Hs pitch (float2), odd: conflict-free row-strided LDS.64
-  static constexpr int QX = TX | 1;
+  static constexpr int SHIFT = (64 * 1024 - R) & 3;  // (x0 - R) mod 4 for x0 % 64 == 0
   static constexpr int BX = 8, BY = 8;               // outputs per x-pass / y-pass item
-  static constexpr size_t kHsBytes = ((size_t)NP * WY * PX * sizeof(float2) + 127) & ~(size_t)127;
-  static constexpr size_t kXsBytes = ((size_t)NP * WY * QX * sizeof(float2) + 127) & ~(size_t)127;
-  static constexpr size_t kTile = ((size_t)BOXX * WY * sizeof(float) + 127) & ~(size_t)127;
-  static constexpr size_t kSmem = kHsBytes + kXsBytes + 2 * kTile + 16;
   // interior Heaviside: pairs of raw columns [C0, C0 + 2*NPR) cover [SHIFT, SHIFT + WX)
   static constexpr int C0 = SHIFT & ~1;
   static constexpr int NPR = (SHIFT + WX - C0 + 1) / 2;
+  // Hs [NP][WY][PH]: H pairs of the haloed tile, raw-column indexed; PH even so a
+  // pair of voxels is one aligned 16-byte store (the y pass reads it along x).
+  static constexpr int PH = (C0 + 2 * NPR + 1) & ~1;
+  // Ys [NP][TY][PY]: y-pass output on the WX window columns; PY odd so the x pass
+  // (lanes walk rows) hits 16 distinct bank pairs per half-warp.
+  static constexpr int PY = WX | 1;
+  // Os [NP][TY][PO]: x-pass output staging for coalesced 16-byte global stores;
+  // PO = TX + 2 makes the row-strided 16-byte stores conflict-free.
+  static constexpr int PO = TX + 2;
+  static constexpr size_t kHsBytes = ((size_t)NP * WY * PH * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kYsBytes = ((size_t)NP * TY * PY * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kOsBytes = ((size_t)NP * TY * PO * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kTile = ((size_t)BOXX * WY * sizeof(float) + 127) & ~(size_t)127;
+  // Os gets its own space when two CTAs still fit an SM; otherwise it aliases
+  // Hs (free after the y pass) at the cost of one more barrier per plane.
+  static constexpr bool kOsAlias = kHsBytes + kYsBytes + kOsBytes + 2 * kTile + 16 > 112 * 1024 &&
+                                   kOsBytes <= kHsBytes;
+  static constexpr size_t kSmem = kHsBytes + kYsBytes + (kOsAlias ? 0 : kOsBytes) + 2 * kTile + 16;
   static constexpr int RG = NT / NPR;                     // row groups of phase A
   static constexpr int RITER = (WY + RG - 1) / RG;        // rows per phase-A thread
-  static constexpr int XIT = (NP * WY * (TX / BX) + NT - 1) / NT;  // x-pass items per thread
-  static constexpr int YIT = (NP * TX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
+  static constexpr int YIT = (NP * WX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
+  static constexpr int XIT = (NP * TY * (TX / BX) + NT - 1) / NT;  // x-pass items per thread
+  static constexpr int OIT = (NP * TY * TX / 2 + NT - 1) / NT;     // copy-out float4 per thread
 };
 
 template <int R, int NP, int TY, bool EDGE>
@@ -110,11 +126,13 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
                                         const CUtensorMap* map_phi, const CUtensorMap* map_img,
                                         unsigned char* smem) {
   using C = XY2<R, NP, TY>;
-  float2* Hs = reinterpret_cast<float2*>(smem);                                // [NP][WY][PX]
-  float2* Xs = reinterpret_cast<float2*>(smem + C::kHsBytes);                  // [NP][WY][QX]
-  float* Tphi = reinterpret_cast<float*>(smem + C::kHsBytes + C::kXsBytes);    // [WY][BOXX]
+  float2* Hs = reinterpret_cast<float2*>(smem);                                         // [NP][WY][PH]
+  float2* Ys = reinterpret_cast<float2*>(smem + C::kHsBytes);                           // [NP][TY][PY]
+  float2* Os = C::kOsAlias ? Hs : reinterpret_cast<float2*>(smem + C::kHsBytes + C::kYsBytes);  // [NP][TY][PO]
+  float* Tphi =
+      reinterpret_cast<float*>(smem + C::kHsBytes + C::kYsBytes + (C::kOsAlias ? 0 : C::kOsBytes));  // [WY][BOXX]
   float* Timg = Tphi + C::kTile / sizeof(float);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kHsBytes + C::kXsBytes + 2 * C::kTile);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Tphi) + 2 * C::kTile);
   const int tid = threadIdx.x;
   // Box origin: (x0 - R) rounded down to 16 bytes, y0 - R.  Starts may be
   // negative (TMA zero-fills outside the volume; only a non-16-byte-aligned x
@@ -129,38 +147,50 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
   const bool a_on = a_rg < C::RG;
   const bool a_last = a_rg + (C::RITER - 1) * C::RG < C::WY;
   const float* Ta = Tphi + a_rg * C::BOXX + C::C0 + 2 * a_pc;
-  float2* Ha = Hs + a_rg * C::PX + C::C0 + 2 * a_pc;
-  // phase B items tid + i*NT -> (np, sx, ry)
+  float2* Ha = Hs + a_rg * C::PH + C::C0 + 2 * a_pc;
+  // phase B (y pass) items tid + i*NT -> (np, sy, cx): column cx of the window,
+  // outputs sy*BY .. sy*BY+7; lanes walk cx.
+  int ysrc[C::YIT], ydst[C::YIT];
+  constexpr int SEGY = TY / C::BY;
+#pragma unroll
+  for (int i = 0; i < C::YIT; ++i) {
+    const int it = min(tid + i * C::NT, NP * C::WX * SEGY - 1);
+    const int np = it / (C::WX * SEGY);
+    const int rem = it - np * C::WX * SEGY;
+    const int sy = rem / C::WX, cx = rem - sy * C::WX;
+    ysrc[i] = np * C::WY * C::PH + (sy * C::BY) * C::PH + C::SHIFT + cx;
+    ydst[i] = np * TY * C::PY + (sy * C::BY) * C::PY + cx;
+  }
+  const bool y_last = tid + (C::YIT - 1) * C::NT < NP * C::WX * SEGY;
+  // phase C (x pass) items -> (np, sx, row): lanes walk rows
   int xsrc[C::XIT], xdst[C::XIT];
   constexpr int SEGX = C::TX / C::BX;
 #pragma unroll
   for (int i = 0; i < C::XIT; ++i) {
-    const int it = min(tid + i * C::NT, NP * C::WY * SEGX - 1);
-    const int np = it / (C::WY * SEGX);
-    const int rem = it - np * C::WY * SEGX;
-    const int sx = rem / C::WY, ry = rem - sx * C::WY;
-    xsrc[i] = np * C::WY * C::PX + ry * C::PX + C::SHIFT + sx * C::BX;
-    xdst[i] = np * C::WY * C::QX + ry * C::QX + sx * C::BX;
+    const int it = min(tid + i * C::NT, NP * TY * SEGX - 1);
+    const int np = it / (TY * SEGX);
+    const int rem = it - np * TY * SEGX;
+    const int sx = rem / TY, row = rem - sx * TY;
+    xsrc[i] = np * TY * C::PY + row * C::PY + sx * C::BX;
+    xdst[i] = np * TY * C::PO + row * C::PO + sx * C::BX;
   }
-  const bool x_last = tid + (C::XIT - 1) * C::NT < NP * C::WY * SEGX;
-  // phase C items tid + i*NT -> (np, sy, cx)
-  int ysrc[C::YIT], ygx[C::YIT], ygy[C::YIT];
-  bool ynp[C::YIT];
-  size_t yout[C::YIT];
-  constexpr int SEGY = TY / C::BY;
+  const bool x_last = tid + (C::XIT - 1) * C::NT < NP * TY * SEGX;
+  // phase D (copy-out) float4 items -> (np, row, column pair)
+  int osrc[C::OIT];
+  size_t odst[C::OIT];
+  bool o_np[C::OIT], o_ok[C::OIT];
 #pragma unroll
-  for (int i = 0; i < C::YIT; ++i) {
-    const int it = min(tid + i * C::NT, NP * C::TX * SEGY - 1);
-    const int np = it / (C::TX * SEGY);
-    const int rem = it - np * C::TX * SEGY;
-    const int sy = rem / C::TX, cx = rem - sy * C::TX;
-    ysrc[i] = np * C::WY * C::QX + (sy * C::BY) * C::QX + cx;
-    ynp[i] = np != 0;
-    ygx[i] = x0 + cx;
-    ygy[i] = y0 + sy * C::BY;
-    yout[i] = (size_t)min(ygy[i], g.ny - 1) * g.nx + min(ygx[i], g.nx - 1);
+  for (int i = 0; i < C::OIT; ++i) {
+    const int it = min(tid + i * C::NT, NP * TY * C::TX / 2 - 1);
+    const int np = it / (TY * C::TX / 2);
+    const int rem = it - np * TY * C::TX / 2;
+    const int row = rem / (C::TX / 2), cp = rem - row * (C::TX / 2);
+    osrc[i] = np * TY * C::PO + row * C::PO + 2 * cp;
+    const int gx = x0 + 2 * cp, gy = y0 + row;
+    o_np[i] = np != 0;
+    o_ok[i] = tid + i * C::NT < NP * TY * C::TX / 2 && (!EDGE || (gx < g.nx && gy < g.ny));
+    odst[i] = (size_t)min(gy, g.ny - 1) * g.nx + min(gx, g.nx - 2);
   }
-  const bool y_last = tid + (C::YIT - 1) * C::NT < NP * C::TX * SEGY;
 
   auto issue = [&](int z) {
     mbar_expect_tx(bar, (uint32_t)(2 * C::BOXX * C::WY * sizeof(float)));
@@ -201,8 +231,8 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
       __syncthreads();
     }
     // ---- Phase A: Heaviside fields of the haloed tile -> Hs.  Pairs of raw
-    // columns (c, c+1), c even: one LDS.64 of phi and of I each.  Thread
-    // (rg, pc) owns pair column pc of rows rg, rg + RG, ... (constant offsets).
+    // columns (c, c+1), c even: one LDS.64 of phi and of I each, one 16-byte
+    // store.  Thread (rg, pc) owns pair column pc of rows rg, rg + RG, ...
     if (a_on) {
 #pragma unroll
       for (int i = 0; i < C::RITER; ++i) {
@@ -213,13 +243,10 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
           float2 hm, hp;
           heaviside2<NP == 2>(pv, inv_eps, hm, hp);
           const float2 hmi = f2mul(hm, iv);
-          float2* d = Ha + ro * C::PX;
-          d[0] = make_float2(hm.x, hmi.x);
-          d[1] = make_float2(hm.y, hmi.y);
+          *reinterpret_cast<float4*>(Ha + ro * C::PH) = make_float4(hm.x, hmi.x, hm.y, hmi.y);
           if (NP == 2) {
             const float2 hpi = f2mul(hp, iv);
-            d[C::WY * C::PX] = make_float2(hp.x, hpi.x);
-            d[C::WY * C::PX + 1] = make_float2(hp.y, hpi.y);
+            *reinterpret_cast<float4*>(Ha + C::WY * C::PH + ro * C::PH) = make_float4(hp.x, hpi.x, hp.y, hpi.y);
           }
         }
       }
@@ -231,53 +258,69 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
       issue(z + 1);
     }
 
-    // ---- Phase B: x pass, BX consecutive outputs per item; lanes walk rows
-    // so a half-warp reads 16 rows of the odd-pitched tile (no bank conflicts).
+    // ---- Phase B: y pass on the WX window columns (the first pass carries the
+    // x halo: WX/TX < WY/TY).  BY outputs down a column, lanes walk x.
 #pragma unroll
-    for (int i = 0; i < C::XIT; ++i) {
-      if (i < C::XIT - 1 || x_last) {
-        const float2* src = Hs + xsrc[i];
-        float2 v[C::BX + 2 * R];
+    for (int i = 0; i < C::YIT; ++i) {
+      if (i < C::YIT - 1 || y_last) {
+        const float2* src = Hs + ysrc[i];
+        float2 v[C::BY + 2 * R];
 #pragma unroll
-        for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
-        float2* dst = Xs + xdst[i];
+        for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::PH];
+        float2* dst = Ys + ydst[i];
 #pragma unroll
-        for (int b = 0; b < C::BX; ++b) {
+        for (int b = 0; b < C::BY; ++b) {
           float2 acc = fmul2(taps.w[0], v[b]);
 #pragma unroll
           for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-          dst[b] = acc;
+          dst[b * C::PY] = acc;
         }
       }
     }
     __syncthreads();
 
-    // ---- Phase C: y pass, BY consecutive outputs down a column; lanes walk x.
+    // ---- Phase C: x pass, BX consecutive outputs per item; lanes walk rows of
+    // the odd-pitched Ys.  Outputs to the staging tile Os.
+#pragma unroll
+    for (int i = 0; i < C::XIT; ++i) {
+      if (i < C::XIT - 1 || x_last) {
+        const float2* src = Ys + xsrc[i];
+        float2 v[C::BX + 2 * R];
+#pragma unroll
+        for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
+        float2 o[C::BX];
+#pragma unroll
+        for (int b = 0; b < C::BX; ++b) {
+          float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+          o[b] = acc;
+        }
+        float4* dst = reinterpret_cast<float4*>(Os + xdst[i]);
+#pragma unroll
+        for (int b = 0; b < C::BX / 2; ++b) dst[b] = make_float4(o[2 * b].x, o[2 * b].y, o[2 * b + 1].x, o[2 * b + 1].y);
+      }
+    }
+    __syncthreads();
+
+    // ---- Phase D: coalesced 16-byte stores of P (two voxels per store)
     {
       float2* Pz0 = P0 + (size_t)(z - g.zb) * (size_t)g.plane;
       float2* Pz1 = NP == 2 ? P1 + (size_t)(z - g.zb) * (size_t)g.plane : nullptr;
 #pragma unroll
-      for (int i = 0; i < C::YIT; ++i) {
-        if (i < C::YIT - 1 || y_last) {
-          const float2* src = Xs + ysrc[i];
-          float2 v[C::BY + 2 * R];
-#pragma unroll
-          for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::QX];
-          float2* Pz = (NP == 2 && ynp[i]) ? Pz1 : Pz0;
-          float2* out = Pz + yout[i];
-#pragma unroll
-          for (int b = 0; b < C::BY; ++b) {
-            float2 acc = fmul2(taps.w[0], v[b]);
-#pragma unroll
-            for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-            if (!EDGE || (ygx[i] < g.nx && ygy[i] + b < g.ny)) out[(size_t)b * g.nx] = acc;
-          }
+      for (int i = 0; i < C::OIT; ++i) {
+        if (o_ok[i]) {
+          const float4 v = *reinterpret_cast<const float4*>(Os + osrc[i]);
+          float2* Pz = (NP == 2 && o_np[i]) ? Pz1 : Pz0;
+          *reinterpret_cast<float4*>(Pz + odst[i]) = v;
         }
       }
     }
-    // next plane's phase A rewrites Hs (last read in phase B, before the
-    // barrier above) and phase B rewrites Xs only after phase A's barrier,
-    // which every thread reaches after finishing this phase C.
+    if (C::kOsAlias) __syncthreads();  // Os == Hs: copy-out done before phase A
+    // Next plane: phase A rewrites Hs (last read in phase B, two barriers
+    // ago), phase B rewrites Ys (last read in phase C, before the barrier
+    // above) after phase A's barrier, and phase C rewrites Os only after
+    // phase B's barrier, which every thread reaches after its phase D.
   }
 }
 
