@@ -203,6 +203,12 @@ typedef struct rsfg_phantom_spec {
 void rsfg_phantom_default(rsfg_phantom_spec* s);
 /* Tube-network image (perturbed) and ground-truth mask, host buffers. */
 int rsfg_phantom(const rsfg_phantom_spec* s, float* image, float* gt_mask);
+/* Same generator with the per-voxel work on the GPU:
+ * DEVICE buffers of nx*ny*nz floats on `device` (d_gt_mask may be NULL).
+ * Centerlines are drawn on the host (serial RNG); the distance raster, blur
+ * and noise run on the device.  launches (may be NULL) = kernels launched. */
+int rsfg_phantom_device(const rsfg_phantom_spec* s, float* d_image, float* d_gt_mask, int32_t device,
+                        int64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     gaussian_kernel,
     init_evolution,
     phantom,
+    phantom_device,
     threshold_phi0,
 )
 from ._lib import LIB_PATH, load  # noqa: F401

@@ -139,6 +139,7 @@ SIGNATURES = {
     "rsfg_slab_destroy": (None, [VP]),
     "rsfg_phantom_default": (None, [P(rsfg_phantom_spec)]),
     "rsfg_phantom": (C.c_int, [P(rsfg_phantom_spec), FP, FP]),
+    "rsfg_phantom_device": (C.c_int, [P(rsfg_phantom_spec), VP, VP, I32, P(C.c_int64)]),
 }
 
 _lib = None

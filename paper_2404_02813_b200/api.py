@@ -267,6 +267,39 @@ def phantom(nx, ny, nz, n_branches=12, radius_min=2.0, radius_max=4.0, tortuosit
     return img, gt
 
 
+def _phantom_spec(nx, ny, nz, **kw):
+    s = L.rsfg_phantom_spec()
+    L.load().rsfg_phantom_default(C.byref(s))
+    for k, v in kw.items():
+        setattr(s, k, v)
+    s.nx, s.ny, s.nz = nx, ny, nz
+    return s
+
+
+def phantom_device(nx, ny, nz, n_branches=12, radius_min=2.0, radius_max=4.0, tortuosity=0.25, foreground=200.0,
+                   background=50.0, rng_seed=1, tree_connected=True, axial_blur_sigma=0.0, noise_sigma=20.0,
+                   contrast_axis=0, contrast_lo=1.0, contrast_hi=1.0, noise_seed=7, device=0, with_gt=True):
+    """phantom() with the per-voxel work on the GPU.
+
+    Returns (image, gt) as torch CUDA tensors of shape (nz, ny, nx) (gt None if
+    with_gt is False).  Same spec and random streams as phantom(); outputs match
+    it except where device and host libm round differently (vanishingly rare)."""
+    import torch
+    s = _phantom_spec(nx, ny, nz, n_branches=n_branches, radius_min=radius_min, radius_max=radius_max,
+                      tortuosity=tortuosity, foreground=foreground, background=background, rng_seed=rng_seed,
+                      tree_connected=int(tree_connected), axial_blur_sigma=axial_blur_sigma,
+                      noise_sigma=noise_sigma, contrast_axis=contrast_axis, contrast_lo=contrast_lo,
+                      contrast_hi=contrast_hi, noise_seed=noise_seed)
+    dev = torch.device("cuda", device)
+    img = torch.empty((nz, ny, nx), dtype=torch.float32, device=dev)
+    gt = torch.empty_like(img) if with_gt else None
+    torch.cuda.synchronize(dev)
+    n = C.c_int64()
+    check(L.load().rsfg_phantom_device(C.byref(s), img.data_ptr(), gt.data_ptr() if gt is not None else None,
+                                        device, C.byref(n)))
+    return img, gt
+
+
 def threshold_phi0(image, level: float = 125.0, inside: float = -2.0, outside: float = 2.0) -> np.ndarray:
     """Documented threshold initialisation for throughput runs (SURVEY.md 8(d) cfg 4)."""
     return np.where(np.asarray(image) > level, np.float32(inside), np.float32(outside)).astype(np.float32)

@@ -78,6 +78,10 @@ thread_local std::string g_perr;
 
 }  // namespace
 
+struct rsfg_phantom_sample {
+  double x, y, z, r;
+};
+
 extern "C" {
 
 __attribute__((visibility("default"))) void rsfg_phantom_default(rsfg_phantom_spec* s) {
@@ -102,8 +106,12 @@ __attribute__((visibility("default"))) void rsfg_phantom_default(rsfg_phantom_sp
   s->noise_seed = 7;
 }
 
-__attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec* s, float* image, float* gt) {
-  if (!s || !image) return RSFG_ERR_STATE;
+}  // extern "C"
+
+// PhantomSpec::validate / PerturbSpec::validate (phantom.cpp:12-34) and the
+// random-walk centerlines (phantom.cpp:55-112): serial in the RNG, cheap.
+// Returns the swept-ball samples in generation order.
+int phantom_centerlines(const rsfg_phantom_spec* s, std::vector<Sample>& all_out) {
   const int nx = s->nx, ny = s->ny, nz = s->nz;
   // PhantomSpec::validate / PerturbSpec::validate (phantom.cpp:12-34)
   if (nx <= 0 || ny <= 0 || nz <= 0 || s->n_branches < 0 || s->radius_min < 1.0 ||
@@ -119,8 +127,8 @@ __attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec*
   const double step = 0.5;
   const double lox = margin, hix = nx - 1 - margin, loy = margin, hiy = ny - 1 - margin;
   const double loz = flat ? 0.0 : margin, hiz = flat ? 0.0 : nz - 1 - margin;
-  std::vector<std::vector<Sample>> branches;
-  std::vector<Sample> all;
+  std::vector<Sample>& all = all_out;
+  all.clear();
   for (int b = 0; b < s->n_branches; ++b) {
     V3 pos;
     if (s->tree_connected && !all.empty()) {
@@ -160,14 +168,25 @@ __attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec*
       pos = {std::clamp(pos.x + step * dir.x, lox, hix), std::clamp(pos.y + step * dir.y, loy, hiy),
              flat ? 0.0 : std::clamp(pos.z + step * dir.z, loz, hiz)};
     }
-    branches.push_back(path);
     all.insert(all.end(), path.begin(), path.end());
   }
+  return RSFG_OK;
+}
+
+extern "C" {
+
+__attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec* s, float* image, float* gt) {
+  if (!s || !image) return RSFG_ERR_STATE;
+  std::vector<Sample> all;
+  if (int rc = phantom_centerlines(s, all)) return rc;
+  const int nx = s->nx, ny = s->ny, nz = s->nz;
+  const bool flat = nz == 1;
 
   const size_t n = (size_t)nx * ny * nz;
   std::vector<float> dist(n, std::numeric_limits<float>::max());
-  for (const auto& path : branches)
-    for (const Sample& q : path) {
+  // Order-independent min over samples (the reference rasterises branch by
+  // branch, phantom.cpp:113-137; min is exact in any order).
+  for (const Sample& q : all) {
       const int x0 = std::max(0, (int)std::floor(q.p.x - q.r - 1.5));
       const int x1 = std::min(nx - 1, (int)std::ceil(q.p.x + q.r + 1.5));
       const int y0 = std::max(0, (int)std::floor(q.p.y - q.r - 1.5));
@@ -182,7 +201,7 @@ __attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec*
             float& cur = dist[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * z)];
             cur = std::min(cur, d);
           }
-    }
+  }
 
   std::vector<float> img(n);
   const float f = s->foreground, bgv = s->background;
@@ -233,3 +252,12 @@ __attribute__((visibility("default"))) int rsfg_phantom(const rsfg_phantom_spec*
 }
 
 }  // extern "C"
+
+// Centerline samples as plain (x, y, z, r) doubles for the device rasteriser.
+int rsfg_phantom_samples_host(const rsfg_phantom_spec* s, std::vector<rsfg_phantom_sample>& out) {
+  std::vector<Sample> all;
+  if (int rc = phantom_centerlines(s, all)) return rc;
+  out.resize(all.size());
+  for (size_t i = 0; i < all.size(); ++i) out[i] = {all[i].p.x, all[i].p.y, all[i].p.z, all[i].r};
+  return RSFG_OK;
+}
