@@ -210,6 +210,25 @@ int rsfg_phantom(const rsfg_phantom_spec* s, float* image, float* gt_mask);
 int rsfg_phantom_device(const rsfg_phantom_spec* s, float* d_image, float* d_gt_mask, int32_t device,
                         int64_t* launches);
 
+/* ---- phi0 initialisation (reference seeding.hpp:12-63) --- */
+typedef struct rsfg_blob_params { /* rsf::BlobParams (seeding.hpp:12-21) */
+  double sigma_b;                 /* detection scale, default 3                      */
+  double response_threshold;      /* fraction of the slice max, default 0.1          */
+  double nms_radius;              /* <= 0 means 2 * sigma_b                          */
+  int32_t dark;                   /* Polarity::dark_on_bright                        */
+} rsfg_blob_params;
+void rsfg_blob_params_default(rsfg_blob_params* b);
+
+/* rsf::init_phi (seeding.cpp:221-235) on a DEVICE image: per-slice blob
+ * seeds (detect_seeds, same set and order as the reference), then
+ * d_phi0 = distance to the seeds - seed_radius, the distance being the fixed
+ * point of the reference's Godunov update (fast_sweep_distance).  seeds_xyz
+ * (3 ints per seed) and seeds_resp may be NULL; at most `cap` are written;
+ * *n_seeds gets the full count.  Errors as rsf::param_error / shape_error. */
+int rsfg_init_phi_device(const float* d_image, int32_t nx, int32_t ny, int32_t nz, const rsfg_blob_params* bp,
+                         double seed_radius, float* d_phi0, int32_t device, int32_t* n_seeds, int32_t* seeds_xyz,
+                         float* seeds_resp, int32_t cap, int32_t* iterations);
+
 #ifdef __cplusplus
 }
 #endif

@@ -189,6 +189,27 @@ int rsfref_phantom(int nx, int ny, int nz, int n_branches, double rmin, double r
   })
 }
 
+// detect_seeds (seeding.cpp:83-145): up to cap seeds as x, y, z triples and
+// responses, in the reference's order; *n gets the full count.
+int rsfref_detect_seeds(const float* vol, int nx, int ny, int nz, double sigma_b, double threshold, double nms,
+                        int dark, int* xyz, float* resp, int cap, int* n) {
+  GUARD({
+    rsf::BlobParams bp;
+    bp.sigma_b = sigma_b;
+    bp.response_threshold = threshold;
+    bp.nms_radius = nms;
+    bp.polarity = dark ? rsf::Polarity::dark_on_bright : rsf::Polarity::bright_on_dark;
+    const rsf::SeedSet s = rsf::detect_seeds(make_vol(vol, nx, ny, nz), bp);
+    *n = static_cast<int>(s.points.size());
+    for (int k = 0; k < *n && k < cap; ++k) {
+      xyz[3 * k] = s.points[k].x;
+      xyz[3 * k + 1] = s.points[k].y;
+      xyz[3 * k + 2] = s.points[k].z;
+      resp[k] = s.points[k].response;
+    }
+  })
+}
+
 // init_phi (seeding.cpp:221-235); returns the seed count through *n_seeds.
 int rsfref_init_phi(const float* vol, int nx, int ny, int nz, double sigma_b, double threshold, double nms,
                     int dark, double seed_radius, float* phi, int* n_seeds) {

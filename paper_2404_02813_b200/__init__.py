@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     extract_mask,
     gaussian_kernel,
     init_evolution,
+    init_phi_device,
     phantom,
     phantom_device,
     threshold_phi0,

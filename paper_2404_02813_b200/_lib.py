@@ -65,6 +65,11 @@ class rsfg_report(C.Structure):
     ]
 
 
+class rsfg_blob_params(C.Structure):
+    _fields_ = [("sigma_b", C.c_double), ("response_threshold", C.c_double), ("nms_radius", C.c_double),
+                ("dark", C.c_int32)]
+
+
 class rsfg_phantom_spec(C.Structure):
     _fields_ = [
         ("nx", C.c_int32),
@@ -140,6 +145,9 @@ SIGNATURES = {
     "rsfg_phantom_default": (None, [P(rsfg_phantom_spec)]),
     "rsfg_phantom": (C.c_int, [P(rsfg_phantom_spec), FP, FP]),
     "rsfg_phantom_device": (C.c_int, [P(rsfg_phantom_spec), VP, VP, I32, P(C.c_int64)]),
+    "rsfg_blob_params_default": (None, [P(rsfg_blob_params)]),
+    "rsfg_init_phi_device": (C.c_int, [VP, I32, I32, I32, P(rsfg_blob_params), C.c_double, VP, I32, P(I32),
+                                       P(I32), FP, I32, P(I32)]),
 }
 
 _lib = None

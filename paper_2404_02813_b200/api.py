@@ -300,6 +300,30 @@ def phantom_device(nx, ny, nz, n_branches=12, radius_min=2.0, radius_max=4.0, to
     return img, gt
 
 
+def init_phi_device(image, sigma_b=3.0, response_threshold=0.1, nms_radius=0.0, dark=False, seed_radius=2.0,
+                    max_seeds=1 << 20):
+    """rsf::init_phi (seeding.cpp:221-235) on the GPU (SURVEY.md 8(f) f2).
+
+    image: torch CUDA float32 tensor (nz, ny, nx).  Returns (phi0 tensor,
+    seeds int32 array (n, 3) of x, y, z, responses float32 array (n,)); the
+    Jacobi iteration count of the distance solve is left in init_phi_device.iterations."""
+    import torch
+    nz, ny, nx = image.shape
+    img = image.contiguous()
+    phi = torch.empty_like(img)
+    b = L.rsfg_blob_params(sigma_b, response_threshold, nms_radius, int(dark))
+    xyz = np.zeros((max_seeds, 3), np.int32)
+    resp = np.zeros(max_seeds, np.float32)
+    n, it = C.c_int32(), C.c_int32()
+    torch.cuda.synchronize(img.device)
+    check(L.load().rsfg_init_phi_device(img.data_ptr(), nx, ny, nz, C.byref(b), seed_radius, phi.data_ptr(),
+                                        img.device.index or 0, C.byref(n), xyz.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        resp.ctypes.data, max_seeds, C.byref(it)))
+    k = min(n.value, max_seeds)
+    init_phi_device.iterations = it.value
+    return phi, xyz[:k].copy(), resp[:k].copy()
+
+
 def threshold_phi0(image, level: float = 125.0, inside: float = -2.0, outside: float = 2.0) -> np.ndarray:
     """Documented threshold initialisation for throughput runs (SURVEY.md 8(d) cfg 4)."""
     return np.where(np.asarray(image) > level, np.float32(inside), np.float32(outside)).astype(np.float32)

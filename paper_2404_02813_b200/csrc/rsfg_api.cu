@@ -1073,4 +1073,59 @@ __attribute__((visibility("default"))) void rsfg_slab_destroy(rsfg_slab* s) {
   delete s;
 }
 
+
+__attribute__((visibility("default"))) void rsfg_blob_params_default(rsfg_blob_params* b) {
+  if (!b) return;
+  b->sigma_b = 3.0;  // seeding.hpp:13-16
+  b->response_threshold = 0.1;
+  b->nms_radius = 0.0;
+  b->dark = 0;
+}
+
+__attribute__((visibility("default"))) int rsfg_init_phi_device(const float* d_image, int32_t nx, int32_t ny,
+                                                                int32_t nz, const rsfg_blob_params* bp,
+                                                                double seed_radius, float* d_phi0, int32_t device,
+                                                                int32_t* n_seeds, int32_t* seeds_xyz,
+                                                                float* seeds_resp, int32_t cap,
+                                                                int32_t* iterations) {
+  rsfg_blob_params b;
+  rsfg_blob_params_default(&b);
+  if (bp) b = *bp;
+  if (!d_image || !d_phi0) return fail(RSFG_ERR_STATE, "init_phi: null buffer");
+  // BlobParams::validate (seeding.cpp:13-19), init_phi (seeding.cpp:223)
+  if (!(b.sigma_b > 0.0)) return fail(RSFG_ERR_PARAM, "BlobParams: sigma_b must be > 0");
+  if (b.response_threshold < 0.0) return fail(RSFG_ERR_PARAM, "BlobParams: response_threshold must be >= 0");
+  const double nms = b.nms_radius > 0.0 ? b.nms_radius : 2.0 * b.sigma_b;
+  if (nms < 1.0) return fail(RSFG_ERR_PARAM, "BlobParams: nms_radius must be >= 1");
+  if (seed_radius < 0.0) return fail(RSFG_ERR_PARAM, "init_phi: seed_radius must be >= 0");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return fail(RSFG_ERR_SHAPE, "volume dims must be positive");
+  if (nx < 5 || ny < 5) return fail(RSFG_ERR_SHAPE, "hessian_det_slice: slice must be at least 5x5");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<rsfg::SeedHost> seeds;
+  long long nl = 0;
+  int rc = rsfg::seed_detect(d_image, nx, ny, nz, b.sigma_b, b.response_threshold, nms, b.dark != 0, seeds, st, &nl);
+  int it = 0;
+  if (!rc && !seeds.empty()) rc = rsfg::seed_distance(nx, ny, nz, seeds, (float)seed_radius, d_phi0, st, &it, &nl);
+  cudaStreamDestroy(st);
+  if (rc == -2) return fail(RSFG_ERR_OOM, "init_phi: out of device memory");
+  if (rc == -3) return fail(RSFG_ERR_PARAM, "init_phi: too many seed candidates");
+  if (rc) return fail(RSFG_ERR_CUDA, std::string("init_phi: CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
+  if (n_seeds) *n_seeds = (int32_t)seeds.size();
+  for (size_t k = 0; k < seeds.size() && (int32_t)k < cap; ++k) {
+    if (seeds_xyz) {
+      seeds_xyz[3 * k] = seeds[k].x;
+      seeds_xyz[3 * k + 1] = seeds[k].y;
+      seeds_xyz[3 * k + 2] = seeds[k].z;
+    }
+    if (seeds_resp) seeds_resp[k] = seeds[k].response;
+  }
+  if (iterations) *iterations = it;
+  if (seeds.empty())
+    return fail(RSFG_ERR_PARAM,
+                "init_phi: no seeds detected; lower response_threshold (or adjust sigma_b) and retry");
+  return RSFG_OK;
+}
+
 }  // extern "C"

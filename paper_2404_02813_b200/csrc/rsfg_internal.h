@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace rsfg {
 
 // A z-slab view of an nx*ny*nz fp32 volume (x fastest) whose buffers hold
@@ -123,5 +125,18 @@ float decode_ordered(unsigned int u);
 unsigned int encode_ordered(float f);
 
 int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st);
+
+// phi0 initialisation (rsfg_seed.cu; reference seeding.cpp:83-235).
+struct SeedHost {
+  int x, y, z;
+  float response;
+};
+// Per-slice Hessian-determinant seeds of a device volume, in the reference's
+// order.  0 ok, -1 CUDA error, -2 out of memory, -3 too many candidates.
+int seed_detect(const float* d_img, int nx, int ny, int nz, double sigma_b, double thr, double nms, bool dark,
+                std::vector<SeedHost>& seeds, cudaStream_t st, long long* launches);
+// d_phi = distance to the seeds (Godunov fixed point) - seed_radius.
+int seed_distance(int nx, int ny, int nz, const std::vector<SeedHost>& seeds, float seed_radius, float* d_phi,
+                  cudaStream_t st, int* iterations, long long* launches);
 
 }  // namespace rsfg

@@ -175,6 +175,8 @@ class RefLib:
                                      C.c_int, C.c_double, C.c_double, C.c_uint64, F32P, F32P]
         L.rsfref_init_phi.argtypes = [F32P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                       C.c_int, C.c_double, F32P, C.POINTER(C.c_int)]
+        L.rsfref_detect_seeds.argtypes = [F32P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                          C.c_int, C.POINTER(C.c_int), F32P, C.c_int, C.POINTER(C.c_int)]
         L.rsfref_dice.argtypes = [F32P, F32P, C.c_int, C.c_int, C.c_int]
         L.rsfref_dice.restype = C.c_double
         L.rsfref_set_workers.argtypes = [C.c_int]
@@ -220,6 +222,17 @@ class RefLib:
         self._check(self.lib.rsfref_init_phi(vol, nx, ny, nz, sigma_b, threshold, nms, int(dark), seed_radius,
                                              phi, C.byref(n)))
         return phi, n.value
+
+    def detect_seeds(self, vol, sigma_b=3.0, threshold=0.1, nms=0.0, dark=False, cap=1 << 20):
+        """(xyz int32 (n, 3), responses float32 (n,)) in the reference's order."""
+        nx, ny, nz = _shape(vol)
+        xyz = np.zeros((cap, 3), np.int32)
+        resp = np.zeros(cap, np.float32)
+        n = C.c_int()
+        self._check(self.lib.rsfref_detect_seeds(vol, nx, ny, nz, sigma_b, threshold, nms, int(dark),
+                                                 xyz.ctypes.data_as(C.POINTER(C.c_int)), resp, cap, C.byref(n)))
+        k = min(n.value, cap)
+        return xyz[:k].copy(), resp[:k].copy()
 
     def dice(self, a, b):
         nx, ny, nz = _shape(a)
