@@ -229,6 +229,43 @@ int rsfg_init_phi_device(const float* d_image, int32_t nx, int32_t ny, int32_t n
                          double seed_radius, float* d_phi0, int32_t device, int32_t* n_seeds, int32_t* seeds_xyz,
                          float* seeds_resp, int32_t cap, int32_t* iterations);
 
+/* ---- curtain tiling around the hot path (tiling.hpp:12-71) -- */
+typedef struct rsfg_tile { /* rsf::TileBox (tiling.hpp:13-17); axes x, y, z */
+  int32_t ix, iy, iz;
+  int32_t core_origin[3], core_extent[3];
+  int32_t pad_origin[3], pad_extent[3];
+} rsfg_tile;
+#define RSFG_MERGE_LINEAR 0 /* rsf::MergeMode (tiling.hpp:26) */
+#define RSFG_MERGE_MINIMUM 1
+#define RSFG_MERGE_MAXIMUM 2
+#define RSFG_MERGE_AVERAGE 3
+typedef struct rsfg_pipeline_options { /* rsf::PipelineOptions (tiling.hpp:41-47) */
+  int32_t global_seeding;
+  int32_t merge;       /* RSFG_MERGE_*                                   */
+  double seed_radius;  /* default 2                                      */
+  int32_t device;
+  int32_t fields;      /* RSFG_FIELDS_2 (default) or RSFG_FIELDS_4       */
+} rsfg_pipeline_options;
+void rsfg_pipeline_options_default(rsfg_pipeline_options* o);
+/* plan_tiles (tiling.cpp:14-59): core tiles of tile size (tx, ty, tz) with a
+ * curtain of ceil(3 max(sigma1, sigma2)); up to cap tiles written. */
+int rsfg_plan_tiles(int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t ty, int32_t tz, double sigma1,
+                    double sigma2, rsfg_tile* tiles, int32_t cap, int32_t* n_tiles, int32_t* curtain);
+/* merge_phi (tiling.cpp:99-193) on the device: d_tile_phis[i] = DEVICE field
+ * of tile i's padded extent (layout of rsfg_plan_tiles with the same tile
+ * size and curtain).  Bit-exact with the reference for identical tiles. */
+int rsfg_merge_phi_device(const float* const* d_tile_phis, int32_t n_tiles, int32_t nx, int32_t ny, int32_t nz,
+                          int32_t tx, int32_t ty, int32_t tz, int32_t curtain, int32_t mode, float* d_out,
+                          int32_t device);
+/* run_pipeline (tiling.cpp:201-275) on one GPU, HOST buffers: every tile is
+ * extracted, seeded (per tile, or by scattering global seeds), initialised
+ * and evolved on the device, then merged on the device.  mask may be NULL.
+ * Warnings (sorted, newline separated) go to `warnings` (may be NULL). */
+int rsfg_run_pipeline(const float* image, int32_t nx, int32_t ny, int32_t nz, const rsfg_params* p,
+                      const rsfg_blob_params* bp, int32_t tx, int32_t ty, int32_t tz,
+                      const rsfg_pipeline_options* o, float* phi, float* mask, char* warnings,
+                      int32_t warnings_cap, int32_t* n_warnings);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,16 +5,18 @@
 // oracle/_ref/librsfref*.so).  It lets tests/ and bench.py's reference arm
 // call the reference's own public C++ API (include/rsf/*.hpp) from ctypes:
 // rsf::evolve / init_evolution / evolve_step / energy / extract_mask, the
-// phantom generator, perturb and init_phi.  No reference source is copied
+// phantom generator, perturb, init_phi, merge_phi and run_pipeline.  No reference source is copied
 // here; every call goes to the reference's compiled code.
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "rsf/phantom.hpp"
 #include "rsf/rsf.hpp"
 #include "rsf/seeding.hpp"
+#include "rsf/tiling.hpp"
 #include "rsf/validation.hpp"
 
 namespace {
@@ -227,6 +229,43 @@ int rsfref_init_phi(const float* vol, int nx, int ny, int nz, double sigma_b, do
 
 double rsfref_dice(const float* a, const float* b, int nx, int ny, int nz) {
   return rsf::dice(make_vol(a, nx, ny, nz), make_vol(b, nx, ny, nz));
+}
+
+// merge_phi (tiling.cpp:99-193) of caller-provided tile fields over
+// plan_tiles((nx, ny, nz), (tx, ty, tz), sigma1, sigma2).
+int rsfref_merge_phi(const float* const* tiles, int n_tiles, int nx, int ny, int nz, int tx, int ty, int tz,
+                     double sigma1, double sigma2, int mode, float* out) {
+  GUARD({
+    const rsf::TileLayout L = rsf::plan_tiles({nx, ny, nz}, {tx, ty, tz}, sigma1, sigma2);
+    if ((int)L.tiles.size() != n_tiles) throw rsf::shape_error("rsfref_merge_phi: tile count");
+    std::vector<rsf::Volume> v;
+    for (int i = 0; i < n_tiles; ++i) {
+      const rsf::Dims& e = L.tiles[i].pad_extent;
+      v.push_back(make_vol(tiles[i], e.nx, e.ny, e.nz));
+    }
+    rsf::Volume m = rsf::merge_phi(v, L, static_cast<rsf::MergeMode>(mode));
+    std::memcpy(out, m.data.data(), m.voxels() * sizeof(float));
+  })
+}
+
+// run_pipeline (tiling.cpp:201-275) with default BlobParams(sigma_b, threshold).
+int rsfref_run_pipeline(const float* image, int nx, int ny, int nz, const RefParams* p, double sigma_b,
+                        double threshold, int tx, int ty, int tz, int global_seeding, int mode, double seed_radius,
+                        float* phi, float* mask, int* n_warnings) {
+  GUARD({
+    rsf::BlobParams bp;
+    bp.sigma_b = sigma_b;
+    bp.response_threshold = threshold;
+    const rsf::TileLayout L = rsf::plan_tiles({nx, ny, nz}, {tx, ty, tz}, p->sigma1, p->sigma2);
+    rsf::PipelineOptions o;
+    o.global_seeding = global_seeding != 0;
+    o.merge = static_cast<rsf::MergeMode>(mode);
+    o.seed_radius = seed_radius;
+    const rsf::PipelineResult r = rsf::run_pipeline(make_vol(image, nx, ny, nz), to_ref(p), bp, L, 0, o);
+    std::memcpy(phi, r.phi.data.data(), r.phi.voxels() * sizeof(float));
+    std::memcpy(mask, r.mask.data.data(), r.mask.voxels() * sizeof(float));
+    *n_warnings = static_cast<int>(r.warnings.size());
+  })
 }
 
 }  // extern "C"

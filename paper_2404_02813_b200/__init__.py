@@ -18,6 +18,9 @@ from .api import (  # noqa: F401
     gaussian_kernel,
     init_evolution,
     init_phi_device,
+    merge_phi_device,
+    plan_tiles,
+    run_pipeline,
     phantom,
     phantom_device,
     threshold_phi0,

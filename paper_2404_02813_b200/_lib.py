@@ -70,6 +70,16 @@ class rsfg_blob_params(C.Structure):
                 ("dark", C.c_int32)]
 
 
+class rsfg_tile(C.Structure):
+    _fields_ = [("ix", C.c_int32), ("iy", C.c_int32), ("iz", C.c_int32), ("core_origin", C.c_int32 * 3),
+                ("core_extent", C.c_int32 * 3), ("pad_origin", C.c_int32 * 3), ("pad_extent", C.c_int32 * 3)]
+
+
+class rsfg_pipeline_options(C.Structure):
+    _fields_ = [("global_seeding", C.c_int32), ("merge", C.c_int32), ("seed_radius", C.c_double),
+                ("device", C.c_int32), ("fields", C.c_int32)]
+
+
 class rsfg_phantom_spec(C.Structure):
     _fields_ = [
         ("nx", C.c_int32),
@@ -146,6 +156,12 @@ SIGNATURES = {
     "rsfg_phantom": (C.c_int, [P(rsfg_phantom_spec), FP, FP]),
     "rsfg_phantom_device": (C.c_int, [P(rsfg_phantom_spec), VP, VP, I32, P(C.c_int64)]),
     "rsfg_blob_params_default": (None, [P(rsfg_blob_params)]),
+    "rsfg_pipeline_options_default": (None, [P(rsfg_pipeline_options)]),
+    "rsfg_plan_tiles": (C.c_int, [I32, I32, I32, I32, I32, I32, C.c_double, C.c_double, P(rsfg_tile), I32, P(I32),
+                                  P(I32)]),
+    "rsfg_merge_phi_device": (C.c_int, [P(VP), I32, I32, I32, I32, I32, I32, I32, I32, I32, VP, I32]),
+    "rsfg_run_pipeline": (C.c_int, [FP, I32, I32, I32, P(rsfg_params), P(rsfg_blob_params), I32, I32, I32,
+                                    P(rsfg_pipeline_options), FP, FP, C.c_char_p, I32, P(I32)]),
     "rsfg_init_phi_device": (C.c_int, [VP, I32, I32, I32, P(rsfg_blob_params), C.c_double, VP, I32, P(I32),
                                        P(I32), FP, I32, P(I32)]),
 }

@@ -324,6 +324,59 @@ def init_phi_device(image, sigma_b=3.0, response_threshold=0.1, nms_radius=0.0, 
     return phi, xyz[:k].copy(), resp[:k].copy()
 
 
+MERGE_MODES = {"linear": 0, "minimum": 1, "maximum": 2, "average": 3}  # rsf::MergeMode (tiling.hpp:26)
+
+
+def plan_tiles(shape, tile_size, sigma1, sigma2=0.0):
+    """rsf::plan_tiles (tiling.cpp:14-59).  shape/tile_size are (nx, ny, nz).
+    Returns (tiles, curtain); each tile a dict of ix, iy, iz and (x, y, z)
+    core_origin / core_extent / pad_origin / pad_extent tuples."""
+    n, c = C.c_int32(), C.c_int32()
+    check(L.load().rsfg_plan_tiles(*shape, *tile_size, sigma1, sigma2, None, 0, C.byref(n), C.byref(c)))
+    buf = (L.rsfg_tile * n.value)()
+    check(L.load().rsfg_plan_tiles(*shape, *tile_size, sigma1, sigma2, buf, n.value, C.byref(n), C.byref(c)))
+    tiles = [{"ix": t.ix, "iy": t.iy, "iz": t.iz, "core_origin": tuple(t.core_origin),
+              "core_extent": tuple(t.core_extent), "pad_origin": tuple(t.pad_origin),
+              "pad_extent": tuple(t.pad_extent)} for t in buf]
+    return tiles, c.value
+
+
+def merge_phi_device(tile_phis, shape, tile_size, curtain, mode="linear", device=0):
+    """rsf::merge_phi (tiling.cpp:99-193) on the GPU.  tile_phis: torch CUDA
+    tensors of each tile's padded extent (nz, ny, nx), in plan_tiles order."""
+    import torch
+    nx, ny, nz = shape
+    ts = [t.contiguous() for t in tile_phis]
+    out = torch.empty((nz, ny, nx), dtype=torch.float32, device=ts[0].device)
+    ptrs = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    torch.cuda.synchronize(out.device)
+    check(L.load().rsfg_merge_phi_device(ptrs, len(ts), nx, ny, nz, *tile_size, curtain, MERGE_MODES[mode],
+                                         out.data_ptr(), device))
+    return out
+
+
+def run_pipeline(vol, p: "RsfParams", tile_size, *, sigma_b=3.0, response_threshold=0.1, nms_radius=0.0,
+                 dark=False, global_seeding=False, merge="linear", seed_radius=2.0, fields=2, device=0):
+    """rsf::run_pipeline (tiling.cpp:201-275) on one GPU: returns (phi, mask,
+    warnings) as host arrays / list of strings."""
+    vol = np.ascontiguousarray(vol, np.float32)
+    nz, ny, nx = vol.shape
+    phi = np.empty_like(vol)
+    mask = np.empty_like(vol)
+    b = L.rsfg_blob_params(sigma_b, response_threshold, nms_radius, int(dark))
+    o = L.rsfg_pipeline_options()
+    L.load().rsfg_pipeline_options_default(C.byref(o))
+    o.global_seeding, o.merge, o.seed_radius, o.device, o.fields = (int(global_seeding), MERGE_MODES[merge],
+                                                                    seed_radius, device, fields)
+    cp = p.to_c()
+    warn = C.create_string_buffer(1 << 16)
+    nw = C.c_int32()
+    check(L.load().rsfg_run_pipeline(_ptr(vol), nx, ny, nz, C.byref(cp), C.byref(b), *tile_size, C.byref(o),
+                                     _ptr(phi), _ptr(mask), warn, len(warn), C.byref(nw)))
+    lines = [w for w in warn.value.decode().split("\n") if w]
+    return phi, mask, lines
+
+
 def threshold_phi0(image, level: float = 125.0, inside: float = -2.0, outside: float = 2.0) -> np.ndarray:
     """Documented threshold initialisation for throughput runs (SURVEY.md 8(d) cfg 4)."""
     return np.where(np.asarray(image) > level, np.float32(inside), np.float32(outside)).astype(np.float32)

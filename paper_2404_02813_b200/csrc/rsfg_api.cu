@@ -90,6 +90,10 @@ constexpr int kSlots = 64;  // per-iteration counter ring
 
 }  // namespace
 
+namespace rsfg {
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace rsfg
+
 // ------------------------------------------------------------------ engine
 struct rsfg_slab {
   int dev = 0;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
 #include <vector>
 
 namespace rsfg {
@@ -125,6 +126,9 @@ float decode_ordered(unsigned int u);
 unsigned int encode_ordered(float f);
 
 int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st);
+
+// Sets the calling thread's rsfg_last_error() message (rsfg_api.cu).
+void set_error(const std::string& msg);
 
 // phi0 initialisation (rsfg_seed.cu; reference seeding.cpp:83-235).
 struct SeedHost {

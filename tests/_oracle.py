@@ -177,6 +177,11 @@ class RefLib:
                                       C.c_int, C.c_double, F32P, C.POINTER(C.c_int)]
         L.rsfref_detect_seeds.argtypes = [F32P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                           C.c_int, C.POINTER(C.c_int), F32P, C.c_int, C.POINTER(C.c_int)]
+        L.rsfref_merge_phi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, F32P]
+        L.rsfref_run_pipeline.argtypes = [F32P, C.c_int, C.c_int, C.c_int, C.POINTER(Params), C.c_double,
+                                          C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          F32P, F32P, C.POINTER(C.c_int)]
         L.rsfref_dice.argtypes = [F32P, F32P, C.c_int, C.c_int, C.c_int]
         L.rsfref_dice.restype = C.c_double
         L.rsfref_set_workers.argtypes = [C.c_int]
@@ -233,6 +238,25 @@ class RefLib:
                                                  xyz.ctypes.data_as(C.POINTER(C.c_int)), resp, cap, C.byref(n)))
         k = min(n.value, cap)
         return xyz[:k].copy(), resp[:k].copy()
+
+    def merge_phi(self, tiles, shape, tile_size, sigma1, sigma2=0.0, mode=0):
+        """merge_phi over plan_tiles(shape (nx, ny, nz), tile_size, sigma1, sigma2)."""
+        nx, ny, nz = shape
+        keep = [np.ascontiguousarray(t, np.float32) for t in tiles]
+        ptrs = (C.c_void_p * len(keep))(*[t.ctypes.data for t in keep])
+        out = np.empty((nz, ny, nx), np.float32)
+        self._check(self.lib.rsfref_merge_phi(ptrs, len(keep), nx, ny, nz, *tile_size, sigma1, sigma2, mode, out))
+        return out
+
+    def run_pipeline(self, vol, p, tile_size, sigma_b=3.0, threshold=0.1, global_seeding=False, mode=0,
+                     seed_radius=2.0):
+        nx, ny, nz = _shape(vol)
+        phi = np.empty_like(vol)
+        mask = np.empty_like(vol)
+        nw = C.c_int()
+        self._check(self.lib.rsfref_run_pipeline(vol, nx, ny, nz, C.byref(p), sigma_b, threshold, *tile_size,
+                                                 int(global_seeding), mode, seed_radius, phi, mask, C.byref(nw)))
+        return phi, mask, nw.value
 
     def dice(self, a, b):
         nx, ny, nz = _shape(a)
