@@ -36,6 +36,7 @@ extern "C" {
 #define RSFG_ERR_COMM 5
 #define RSFG_ERR_OOM 6
 #define RSFG_ERR_STATE 7 /* misuse: null handle, invalidated state, ...        */
+#define RSFG_ERR_IO 8    /* rsf::io_error (volume_io.cpp:24-137)              */
 
 /* Field-for-field rsf::RsfParams (rsf.hpp:13-26); defaults via
  * rsfg_params_default().  north_star names: sigma -> sigma1 (+sigma2),
@@ -265,6 +266,25 @@ int rsfg_run_pipeline(const float* image, int32_t nx, int32_t ny, int32_t nz, co
                       const rsfg_blob_params* bp, int32_t tx, int32_t ty, int32_t tz,
                       const rsfg_pipeline_options* o, float* phi, float* mask, char* warnings,
                       int32_t warnings_cap, int32_t* n_warnings);
+
+/* ---- volume I/O and overlap metrics ------------------ */
+/* read_volume's header (volume_io.cpp:24-76): dims, spacing, payload width. */
+int rsfg_volume_info(const char* header, int32_t* nx, int32_t* ny, int32_t* nz, double* spacing3,
+                     int32_t* elem_bytes);
+/* read_volume (volume_io.cpp:24-113) into a DEVICE buffer of >= capacity
+ * floats: the payload crosses PCIe in its stored width (u8/u16/f32), chunked
+ * and double-buffered, and is converted on the device (u16 rescaled onto
+ * [0, 255]).  range2 (may be NULL) = header range or min/max.  h2d_bytes
+ * (may be NULL) = bytes copied to the device. */
+int rsfg_read_volume_device(const char* header, float* d_out, int64_t capacity, int32_t device, float* range2,
+                            int64_t* h2d_bytes);
+/* write_volume (volume_io.cpp:115-137) of a DEVICE field (f32 payload). */
+int rsfg_write_volume_device(const char* header, const float* d_v, int32_t nx, int32_t ny, int32_t nz,
+                             const double* spacing3, const float* range2, int32_t device);
+/* dice / jaccard (validation.cpp:41-52) of two DEVICE volumes (> 0.5 is
+ * foreground, exact counts). */
+int rsfg_overlap_device(const float* d_a, const float* d_b, int64_t n, int32_t device, double* dice,
+                        double* jaccard);
 
 #ifdef __cplusplus
 }

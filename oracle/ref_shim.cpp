@@ -18,6 +18,7 @@
 #include "rsf/seeding.hpp"
 #include "rsf/tiling.hpp"
 #include "rsf/validation.hpp"
+#include "rsf/volume_io.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -49,8 +50,9 @@ rsf::Volume make_vol(const float* d, int nx, int ny, int nz) {
   return v;
 }
 
-// 0 ok, 1 param, 2 shape, 3 blowup, 7 other
+// 0 ok, 1 param, 2 shape, 3 blowup, 8 io, 7 other
 int code_of(const std::exception& e) {
+  if (dynamic_cast<const rsf::io_error*>(&e)) return 8;
   if (dynamic_cast<const rsf::param_error*>(&e)) return 1;
   if (dynamic_cast<const rsf::shape_error*>(&e)) return 2;
   if (dynamic_cast<const rsf::blowup_error*>(&e)) return 3;
@@ -265,6 +267,17 @@ int rsfref_run_pipeline(const float* image, int nx, int ny, int nz, const RefPar
     std::memcpy(phi, r.phi.data.data(), r.phi.voxels() * sizeof(float));
     std::memcpy(mask, r.mask.data.data(), r.mask.voxels() * sizeof(float));
     *n_warnings = static_cast<int>(r.warnings.size());
+  })
+}
+
+// read_volume (volume_io.cpp:24-113) into out (capacity cap floats).
+int rsfref_read_volume(const char* header, float* out, long cap, int* nx, int* ny, int* nz, float* range2) {
+  GUARD({
+    rsf::Volume v = rsf::read_volume(header);
+    *nx = v.dims.nx, *ny = v.dims.ny, *nz = v.dims.nz;
+    if ((long)v.voxels() > cap) throw rsf::shape_error("rsfref_read_volume: capacity");
+    std::memcpy(out, v.data.data(), v.voxels() * sizeof(float));
+    range2[0] = v.value_range->first, range2[1] = v.value_range->second;
   })
 }
 

@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     ParamError,
     RsfParams,
     ShapeError,
+    VolumeIOError,
     dice,
     energy,
     evolve,
@@ -19,6 +20,9 @@ from .api import (  # noqa: F401
     init_evolution,
     init_phi_device,
     merge_phi_device,
+    overlap_device,
+    read_volume_device,
+    write_volume_device,
     plan_tiles,
     run_pipeline,
     phantom,

@@ -21,6 +21,7 @@ RSFG_ERR_CUDA = 4
 RSFG_ERR_COMM = 5
 RSFG_ERR_OOM = 6
 RSFG_ERR_STATE = 7
+RSFG_ERR_IO = 8
 
 
 class rsfg_params(C.Structure):
@@ -157,6 +158,10 @@ SIGNATURES = {
     "rsfg_phantom_device": (C.c_int, [P(rsfg_phantom_spec), VP, VP, I32, P(C.c_int64)]),
     "rsfg_blob_params_default": (None, [P(rsfg_blob_params)]),
     "rsfg_pipeline_options_default": (None, [P(rsfg_pipeline_options)]),
+    "rsfg_volume_info": (C.c_int, [C.c_char_p, P(I32), P(I32), P(I32), P(C.c_double), P(I32)]),
+    "rsfg_read_volume_device": (C.c_int, [C.c_char_p, VP, C.c_int64, I32, P(C.c_float), P(C.c_int64)]),
+    "rsfg_write_volume_device": (C.c_int, [C.c_char_p, VP, I32, I32, I32, P(C.c_double), P(C.c_float), I32]),
+    "rsfg_overlap_device": (C.c_int, [VP, VP, C.c_int64, I32, P(C.c_double), P(C.c_double)]),
     "rsfg_plan_tiles": (C.c_int, [I32, I32, I32, I32, I32, I32, C.c_double, C.c_double, P(rsfg_tile), I32, P(I32),
                                   P(I32)]),
     "rsfg_merge_phi_device": (C.c_int, [P(VP), I32, I32, I32, I32, I32, I32, I32, I32, I32, VP, I32]),

@@ -42,7 +42,12 @@ class CudaError(RsfError):
     pass
 
 
-_ERRORS = {L.RSFG_ERR_PARAM: ParamError, L.RSFG_ERR_SHAPE: ShapeError, L.RSFG_ERR_BLOWUP: BlowupError}
+class VolumeIOError(OSError):
+    """rsf::io_error (volume_io.cpp:24-137)."""
+
+
+_ERRORS = {L.RSFG_ERR_PARAM: ParamError, L.RSFG_ERR_SHAPE: ShapeError, L.RSFG_ERR_BLOWUP: BlowupError,
+           L.RSFG_ERR_IO: VolumeIOError}
 
 
 def check(rc: int) -> None:
@@ -375,6 +380,38 @@ def run_pipeline(vol, p: "RsfParams", tile_size, *, sigma_b=3.0, response_thresh
                                      _ptr(phi), _ptr(mask), warn, len(warn), C.byref(nw)))
     lines = [w for w in warn.value.decode().split("\n") if w]
     return phi, mask, lines
+
+
+def read_volume_device(header, device=0):
+    """rsf::read_volume (volume_io.cpp:24-113) straight into a torch CUDA
+    tensor (nz, ny, nx); returns (volume, spacing (sx, sy, sz), value_range,
+    h2d_bytes)."""
+    import torch
+    nx, ny, nz, eb = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    sp = (C.c_double * 3)()
+    hb = str(header).encode()
+    check(L.load().rsfg_volume_info(hb, C.byref(nx), C.byref(ny), C.byref(nz), sp, C.byref(eb)))
+    out = torch.empty((nz.value, ny.value, nx.value), dtype=torch.float32, device=torch.device("cuda", device))
+    rng = (C.c_float * 2)()
+    moved = C.c_int64()
+    check(L.load().rsfg_read_volume_device(hb, out.data_ptr(), out.numel(), device, rng, C.byref(moved)))
+    return out, tuple(sp), (rng[0], rng[1]), moved.value
+
+
+def write_volume_device(header, vol, spacing=(1.0, 1.0, 1.0), device=0):
+    """rsf::write_volume (volume_io.cpp:115-137) of a torch CUDA tensor."""
+    nz, ny, nx = vol.shape
+    sp = (C.c_double * 3)(*spacing)
+    check(L.load().rsfg_write_volume_device(str(header).encode(), vol.contiguous().data_ptr(), nx, ny, nz, sp, None,
+                                            device))
+
+
+def overlap_device(a, b, device=0):
+    """(dice, jaccard) (validation.cpp:41-52) of two torch CUDA tensors."""
+    d, j = C.c_double(), C.c_double()
+    check(L.load().rsfg_overlap_device(a.contiguous().data_ptr(), b.contiguous().data_ptr(), a.numel(), device,
+                                       C.byref(d), C.byref(j)))
+    return d.value, j.value
 
 
 def threshold_phi0(image, level: float = 125.0, inside: float = -2.0, outside: float = 2.0) -> np.ndarray:

@@ -182,6 +182,8 @@ class RefLib:
         L.rsfref_run_pipeline.argtypes = [F32P, C.c_int, C.c_int, C.c_int, C.POINTER(Params), C.c_double,
                                           C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                           F32P, F32P, C.POINTER(C.c_int)]
+        L.rsfref_read_volume.argtypes = [C.c_char_p, F32P, C.c_long, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), F32P]
         L.rsfref_dice.argtypes = [F32P, F32P, C.c_int, C.c_int, C.c_int]
         L.rsfref_dice.restype = C.c_double
         L.rsfref_set_workers.argtypes = [C.c_int]
@@ -190,7 +192,7 @@ class RefLib:
     def _check(self, rc):
         if rc != 0:
             msg = self.lib.rsfref_last_error().decode()
-            raise {1: ValueError, 2: ValueError, 3: FloatingPointError}.get(rc, RuntimeError)(msg)
+            raise {1: ValueError, 2: ValueError, 3: FloatingPointError, 8: OSError}.get(rc, RuntimeError)(msg)
 
     def set_workers(self, n):
         self.lib.rsfref_set_workers(n)
@@ -257,6 +259,14 @@ class RefLib:
         self._check(self.lib.rsfref_run_pipeline(vol, nx, ny, nz, C.byref(p), sigma_b, threshold, *tile_size,
                                                  int(global_seeding), mode, seed_radius, phi, mask, C.byref(nw)))
         return phi, mask, nw.value
+
+    def read_volume(self, header, cap=1 << 26):
+        out = np.empty(cap, np.float32)
+        nx, ny, nz = C.c_int(), C.c_int(), C.c_int()
+        rng = np.empty(2, np.float32)
+        self._check(self.lib.rsfref_read_volume(str(header).encode(), out, cap, C.byref(nx), C.byref(ny),
+                                                C.byref(nz), rng))
+        return out[:nx.value * ny.value * nz.value].reshape(nz.value, ny.value, nx.value).copy(), tuple(rng)
 
     def dice(self, a, b):
         nx, ny, nz = _shape(a)
