@@ -177,9 +177,15 @@ class _DevView:
 
 
 class DistSlab:
-    """One slab per rank; halo exchange with torch.distributed (NCCL on GPUs)."""
+    """One slab per rank; halo exchange with torch.distributed (NCCL on GPUs).
 
-    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None):
+    transport="device" (default) posts NCCL send/recv on views of the slab's own
+    device buffers, overlapped with the interior work.  transport="host" stages
+    the halo planes through host memory for CPU-only process groups (gloo): it
+    lets several ranks share one GPU, which is how this path is tested on
+    single-GPU machines (tests/test_gpu_distslab.py)."""
+
+    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None, transport="device"):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -194,8 +200,9 @@ class DistSlab:
         self.slab.upload(phi0, I)
         self.stream = torch.cuda.current_stream()
         self.slab.set_stream(self.stream.cuda_stream)
+        self.transport = transport
         lo, hi = self.slab.local_range()
-        t = torch.tensor([-lo, hi], dtype=torch.float32, device="cuda")
+        t = torch.tensor([-lo, hi], dtype=torch.float32, device="cuda" if transport == "device" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         self.slab.init(-float(t[0]), float(t[1]))
 
@@ -207,10 +214,26 @@ class DistSlab:
         return t.as_tensor(_DevView(send, n), device="cuda"), t.as_tensor(_DevView(recv, n), device="cuda")
 
     def step(self):
+        if self.transport == "host":
+            return self._step_host()
         reqs = start_halo_exchange(self.dist, self.rank, self.world, self._views(0), self._views(1))
         self.slab.step_interior()  # overlaps the exchange (no halo needed)
         for q in reqs:
             q.wait()
+        self.slab.step_finish()
+
+    def _step_host(self):
+        self.stream.synchronize()  # the previous step's phi is complete
+        views = [self._views(0), self._views(1)]
+        staged = [(v[0].cpu(), self.torch.empty(v[1].shape, dtype=v[1].dtype)) if v[0] is not None else (None, None)
+                  for v in views]
+        reqs = start_halo_exchange(self.dist, self.rank, self.world, staged[0], staged[1])
+        self.slab.step_interior()
+        for q in reqs:
+            q.wait()
+        for v, st in zip(views, staged):
+            if v[1] is not None:
+                v[1].copy_(st[1])
         self.slab.step_finish()
 
     def phi_owned(self) -> np.ndarray:
