@@ -234,18 +234,26 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
     // columns (c, c+1), c even: one LDS.64 of phi and of I each, one 16-byte
     // store.  Thread (rg, pc) owns pair column pc of rows rg, rg + RG, ...
     if (a_on) {
+      // all of this thread's loads first (the stores below may alias them as
+      // far as the compiler knows), then the packed Heaviside and the stores
+      float2 pv[C::RITER], iv[C::RITER];
+#pragma unroll
+      for (int i = 0; i < C::RITER; ++i) {
+        if (i < C::RITER - 1 || a_last) {
+          pv[i] = *reinterpret_cast<const float2*>(Ta + i * C::RG * C::BOXX);
+          iv[i] = *reinterpret_cast<const float2*>(Ta + C::kTile / sizeof(float) + i * C::RG * C::BOXX);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < C::RITER; ++i) {
         if (i < C::RITER - 1 || a_last) {
           const int ro = i * C::RG;
-          const float2 pv = *reinterpret_cast<const float2*>(Ta + ro * C::BOXX);
-          const float2 iv = *reinterpret_cast<const float2*>(Ta + C::kTile / sizeof(float) + ro * C::BOXX);
           float2 hm, hp;
-          heaviside2<NP == 2>(pv, inv_eps, hm, hp);
-          const float2 hmi = f2mul(hm, iv);
+          heaviside2<NP == 2>(pv[i], inv_eps, hm, hp);
+          const float2 hmi = f2mul(hm, iv[i]);
           *reinterpret_cast<float4*>(Ha + ro * C::PH) = make_float4(hm.x, hmi.x, hm.y, hmi.y);
           if (NP == 2) {
-            const float2 hpi = f2mul(hp, iv);
+            const float2 hpi = f2mul(hp, iv[i]);
             *reinterpret_cast<float4*>(Ha + C::WY * C::PH + ro * C::PH) = make_float4(hp.x, hpi.x, hp.y, hpi.y);
           }
         }
