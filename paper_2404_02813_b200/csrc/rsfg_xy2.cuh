@@ -126,9 +126,12 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
                                         const CUtensorMap* map_phi, const CUtensorMap* map_img,
                                         unsigned char* smem) {
   using C = XY2<R, NP, TY>;
-  float2* Hs = reinterpret_cast<float2*>(smem);                                         // [NP][WY][PH]
-  float2* Ys = reinterpret_cast<float2*>(smem + C::kHsBytes);                           // [NP][TY][PY]
-  float2* Os = C::kOsAlias ? Hs : reinterpret_cast<float2*>(smem + C::kHsBytes + C::kYsBytes);  // [NP][TY][PO]
+  // Hs, Ys and Os are disjoint (Os == Hs only under kOsAlias, whose phases a
+  // barrier separates): restrict lets loads of one item pass stores of another.
+  float2* __restrict__ Hs = reinterpret_cast<float2*>(smem);                            // [NP][WY][PH]
+  float2* __restrict__ Ys = reinterpret_cast<float2*>(smem + C::kHsBytes);              // [NP][TY][PY]
+  float2* __restrict__ Os =
+      C::kOsAlias ? Hs : reinterpret_cast<float2*>(smem + C::kHsBytes + C::kYsBytes);  // [NP][TY][PO]
   float* Tphi =
       reinterpret_cast<float*>(smem + C::kHsBytes + C::kYsBytes + (C::kOsAlias ? 0 : C::kOsBytes));  // [WY][BOXX]
   float* Timg = Tphi + C::kTile / sizeof(float);

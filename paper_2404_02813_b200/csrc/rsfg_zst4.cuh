@@ -260,7 +260,19 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       // plane q+2 (slot (k+4)&7) landed?  Issued for step q-4 / the prologue.
       mbar_wait(bars + ((k + 4) & 7), (uint32_t)((grp + (k >= 4 ? 1 : 0)) & 1));
 
-      // ---- A: own normal at plane q+1 (n_x, n_y -> shared; n_z stays here)
+      // Shared loads first: the output's normals of plane q and static
+      // fields, then the phi of plane q+1 -- ahead of this step's normal
+      // stores, which the compiler must otherwise keep them behind.
+      const float* N0 = Nr + nq + own.n;
+      float nxm, nxp, nym, nyp;
+      if constexpr (!GEN) {
+        nxm = N0[-1], nxp = N0[1], nym = N0[C::NPL - C::NXr], nyp = N0[C::NPL + C::NXr];
+      } else {
+        nxm = N0[kxm], nxp = N0[kxp], nym = N0[C::NPL + kym], nyp = N0[C::NPL + kyp];
+      }
+      const float* K = Kr + ((k + 2) & 7) * C::NK * C::NT + tid;
+      const float ki = K[0];
+      const float k1i = NP == 1 ? K[C::NT] : 0.0f;
       const float* p1 = Pown + o1;
       float xm1, xp1, ym1, yp1;
       if constexpr (GEN) {
@@ -269,6 +281,8 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
         xm1 = p1[-1], xp1 = p1[1], ym1 = p1[-C::BX], yp1 = p1[C::BX];
       }
       const float cp2 = Pown[o2];
+
+      // ---- A: own normal at plane q+1 (n_x, n_y -> shared; n_z stays here)
       float a = xp1 - xm1, bb = yp1 - ym1, cc = cp2 - c0;
       if constexpr (GEN) {
         a *= own.fx;
@@ -276,20 +290,19 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
         cc *= fzq(q + 1);
       }
       const float inv = fminf(rsqrt_approx(fmaf(a, a, fmaf(bb, bb, cc * cc))), inv2floor);
-      Nr[nq1 + own.n] = a * inv;
-      Nr[nq1 + C::NPL + own.n] = bb * inv;
       const float nzp1 = cc * inv;
       if (has_halo) halo_normal(genc, o0, o1, o2, GEN ? fzq(q + 1) : 1.0f, Nr + nq1);
+      Nr[nq1 + own.n] = a * inv;
+      Nr[nq1 + C::NPL + own.n] = bb * inv;
 
       // ---- B: output voxel (x, y, q)
-      const float* N0 = Nr + nq + own.n;
       float kappa;
       if constexpr (!GEN) {
         // kappa = div n (ops.cpp:281-316), doubled convention: 0.5 * sum of central differences
-        kappa = 0.5f * (((N0[1] - N0[-1]) + (N0[C::NPL + C::NXr] - N0[C::NPL - C::NXr])) + (nzp1 - nzm1));
+        kappa = 0.5f * (((nxp - nxm) + (nyp - nym)) + (nzp1 - nzm1));
       } else {
-        const float dx = (N0[kxp] - N0[kxm]) * kfx;
-        const float dy = (N0[C::NPL + kyp] - N0[C::NPL + kym]) * kfy;
+        const float dx = (nxp - nxm) * kfx;
+        const float dy = (nyp - nym) * kfy;
         // z face rule: q == 0 -> n(1) - n(0); q == nz-1 -> n(nz-1) - n(nz-2); factor 2
         const float zp = q + 1 <= nz - 1 ? nzp1 : nz0;
         const float zm = q - 1 >= 0 ? nzm1 : nz0;
@@ -301,8 +314,6 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       // delta_eps (rsf.cpp:96-107)
       const float delta = c.c_delta * rcp_approx(fmaf(c0, c0, c.eps2));
       // region averages r+- and F- - F+ (rsf.cpp:130-148, 164)
-      const float* K = Kr + ((k + 2) & 7) * C::NK * C::NT + tid;
-      const float ki = K[0];
       const float km = kh[0][k].x, kmi = kh[0][k].y;
       float kp, kpi;
       if constexpr (NP == 2) {
@@ -310,7 +321,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
         kpi = kh[NP - 1][k].y;
       } else {
         kp = 1.0f - km;
-        kpi = K[C::NT] - kmi;
+        kpi = k1i - kmi;
       }
       // the floored denominators are >= denom_floor > FLT_MIN: plain rcp.approx
       const float rp = fminf(fmaxf(kpi * rcp_approx(fmaxf(kp, c.denom_floor)), c.i_min), c.i_max);
