@@ -220,8 +220,11 @@ void make_xy2_maps(rsfg_slab* s) {
   s->xy2maps[0].valid = s->xy2maps[1].valid = false;
   const char* off = std::getenv("RSFG_XY2");
   if ((off && off[0] == '0') || !s->fast || (s->nx % 4) != 0) return;
+  // Tile height: 64 x 64 (1 CTA/SM, 16 warps) amortises the Heaviside halo
+  // better at large radii; 64 x 32 (2 CTAs/SM) wins up to R = 12
+  // (profiles/r01_xy2_tile_height.txt).  RSFG_XY2_TY=32|64 overrides.
   const char* ty = std::getenv("RSFG_XY2_TY");
-  s->xy2_ty = (ty && std::atoi(ty) == 64) ? 64 : 32;
+  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 ? 64 : 32);
   int bx = 0, by = 0;
   if (!rsfg::xy2_box(s->t1.r, s->xy2_ty, &bx, &by)) return;
   const int planes = s->ze - s->zb;
