@@ -64,19 +64,19 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 }
 
 // Smoothed step H+ = 1/2 [1 + (2/pi) atan(phi/eps)] and H- = 1 - H+
-// (rsf.cpp:22-25, 89-90).  The side that is small is always evaluated
-// directly (atan(1/t)/pi for t > 1) so both values keep full relative
-// precision in fp32, as the reference's f64 evaluation does.
+// (rsf.cpp:22-25, 89-90), as 1/2 -+ sign(u) A with A = atan(|u|)/pi from the
+// polynomial on q = min(|u|, 1/|u|): A = a (|u| <= 1) or 1/2 - a.  The small
+// side on |u| > 1 is 1/2 - (1/2 - a), off a by one rounding (3e-8 absolute),
+// where delta(phi) <= 1/(pi u^2) makes it negligible.  Same bits as the packed
+// heaviside2 (rsfg_xy2.cuh).
 __device__ __forceinline__ void heaviside_pair(float phi, float inv_eps, float& hm, float& hp) {
   const float u = phi * inv_eps;
   const float t = fabsf(u);
-  const bool far = t > 1.0f;
-  const float a = atan_over_pi(far ? rcp_approx(t) : t);
-  const float small = far ? a : 0.5f - a;
-  const float big = far ? 1.0f - a : 0.5f + a;
-  const bool pos = u >= 0.0f;
-  hm = pos ? small : big;
-  hp = pos ? big : small;
+  const float a = atan_over_pi(fminf(t, rcp_approx(t)));
+  const float A = t > 1.0f ? 0.5f - a : a;
+  const float sA = copysignf(A, u);
+  hm = 0.5f - sA;
+  hp = 0.5f + sA;
 }
 
 // ---- TMA (cp.async.bulk.tensor) + mbarrier, sm_90+/sm_100a PTX

@@ -49,9 +49,8 @@ __device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
 
 // Heaviside pair of two voxels, packed: hm = H-(phi), hp = H+(phi) with
 // H+ = 1/2 [1 + (2/pi) atan(phi/eps)] (rsf.cpp:22-25, 89-90).  Same
-// evaluation as heaviside_pair (rsfg_device.cuh): atan(q)/pi on q = min(t,
-// 1/t) in [0, 1], and the small side of each pair is formed directly (never
-// as 1 - big) so both keep full relative precision.
+// evaluation as heaviside_pair (rsfg_device.cuh), bit for bit: atan(q)/pi on
+// q = min(t, 1/t) in [0, 1].
 template <bool WANT_HP>
 __device__ __forceinline__ void heaviside2(float2 phi, float inv_eps, float2& hm, float2& hp) {
   const float2 u = f2mul(phi, f2s(inv_eps));
@@ -67,19 +66,14 @@ __device__ __forceinline__ void heaviside2(float2 phi, float inv_eps, float2& hm
   p = f2fma(p, x, f2s(-0.10610246658325195f));
   p = f2fma(p, x, f2s(0.31830987334251404f));
   const float2 a = f2mul(p, q);  // atan(q)/pi in [0, 1/4]
-  // sa = sign(u) * a.  near (t <= 1): H- = 1/2 - sa, H+ = 1/2 + sa.
-  // far (t > 1): H- = (u < 0) + sa, H+ = (u >= 0) - sa.
-  const float2 sa = make_float2(copysignf(a.x, u.x), copysignf(a.y, u.y));
-  const bool fx = tx > 1.0f, fy = ty > 1.0f;
-  const bool nx_ = u.x < 0.0f, ny_ = u.y < 0.0f;
-  const float2 m_near = f2add(f2s(0.5f), make_float2(-sa.x, -sa.y));
-  const float2 m_far = f2add(make_float2(nx_ ? 1.0f : 0.0f, ny_ ? 1.0f : 0.0f), sa);
-  hm = make_float2(fx ? m_far.x : m_near.x, fy ? m_far.y : m_near.y);
-  if constexpr (WANT_HP) {
-    const float2 p_near = f2add(f2s(0.5f), sa);
-    const float2 p_far = f2add(make_float2(nx_ ? 0.0f : 1.0f, ny_ ? 0.0f : 1.0f), make_float2(-sa.x, -sa.y));
-    hp = make_float2(fx ? p_far.x : p_near.x, fy ? p_far.y : p_near.y);
-  }
+  // A = atan(t)/pi = far ? 1/2 - a : a; H- = 1/2 - sign(u) A, H+ = 1/2 + sign(u) A.
+  // On the far side the small H is 1/2 - (1/2 - a): exact but for one rounding
+  // of 1/2 - a (3e-8 absolute), where delta(phi) <= 1/(pi t^2) is negligible.
+  const float2 am = f2add(f2s(0.5f), make_float2(-a.x, -a.y));
+  const float2 A = make_float2(tx > 1.0f ? am.x : a.x, ty > 1.0f ? am.y : a.y);
+  const float2 sA = make_float2(copysignf(A.x, u.x), copysignf(A.y, u.y));
+  hm = f2add(f2s(0.5f), make_float2(-sA.x, -sA.y));
+  if constexpr (WANT_HP) hp = f2add(f2s(0.5f), sA);
 }
 
 template <int R, int NP, int TY>
