@@ -7,8 +7,9 @@ A "step" is one RSF iteration (rsf::evolve_step, rsf.cpp:324-357) over the
 whole volume.  Workload (BASELINE.json configs[1], SURVEY.md 8(d) cfg 2):
 512^3 synthetic tube network (reference phantom spec, n_branches 192, noise
 sigma 20), sigma1 = 3 (R = 9), sigma2 = 0, 3d-paper parameters, phi0 =
-threshold initialisation.  N > 1 splits the same volume into z-slabs (strong
-scaling) with per-step NCCL halo exchange (paper_2404_02813_b200/spmd.py).
+threshold initialisation.  N > 1 scales WEAKLY: each GPU owns a 512^3 z-slab
+of a 512x512x(512 N) volume, with per-step NCCL halo exchange
+(paper_2404_02813_b200/spmd.py).
 
 `value`   : device-resident inputs, CUDA events around exactly K steps on the
             launching stream, max over ranks.  Inputs (1.5 GiB working set)
@@ -268,7 +269,7 @@ def bench_single(args):
                    "sample": f"unavailable: {e}"}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference phantom spec, seeded)",
            "config": workload_config(1, args.fields), "roofline": roofline, "step_roofline": step_roofline,
            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
@@ -276,26 +277,54 @@ def bench_single(args):
 
 
 def bench_multi(args):
+    """N > 1: weak scaling.  The volume is 512 x 512 x (512 N) (the cfg-2 tube
+    network with 192 N branches, same density), one 512^3 z-slab per rank
+    (SURVEY.md 8(e)): per-step NCCL halo exchange of R planes each way,
+    overlapped with the owned planes' xy work.  Every rank generates the same
+    volume on its own GPU (device phantom, bit-exact with the reference
+    generator) and uploads only its held planes.  value = all voxels x K steps
+    / max over ranks of the CUDA-event time.  --backend gloo --share-gpu runs
+    the same path with ranks sharing cuda:0 and host-staged halos (1-GPU test
+    boxes)."""
     import torch
     import torch.distributed as dist
     import paper_2404_02813_b200 as rsf
-    from paper_2404_02813_b200.spmd import DistSlab
+    from paper_2404_02813_b200.spmd import DistSlab, Slab
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    img, phi0 = make_inputs()
-    nvox = img.size
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    transport = "device" if args.backend == "nccl" else "host"
+    nz_total = NZ * world
+    spec = dict(PHANTOM)
+    spec["n_branches"] = PHANTOM["n_branches"] * world
+    img, _ = rsf.phantom_device(NX, NY, nz_total, with_gt=False, device=local,
+                                **{k: v for k, v in spec.items() if k not in ("rng_seed", "noise_seed")},
+                                rng_seed=spec["rng_seed"], noise_seed=spec["noise_seed"])
+    phi0 = torch.where(img > 125.0, -2.0, 2.0).to(torch.float32)
+    nvox = NX * NY * nz_total
     p = rsf.RsfParams(sigma1=SIGMA1, sigma2=0.0, max_iters=ITERS_CFG)
-    ds = DistSlab(phi0, img, p, fields=args.fields)
+    ds = DistSlab(phi0, img, p, fields=args.fields, transport=transport)
+    # host copies of this rank's held planes for the e2e leg (outside any timing)
+    zb, ze = ds.slab.zb, ds.slab.ze
+    h_img = torch.empty((nz_total, NY, NX), dtype=torch.float32).numpy()  # untouched planes stay unbacked
+    h_phi = torch.empty((nz_total, NY, NX), dtype=torch.float32).numpy()
+    h_img[zb:ze] = img[zb:ze].cpu().numpy()
+    h_phi[zb:ze] = phi0[zb:ze].cpu().numpy()
+    del img, phi0
+    torch.cuda.empty_cache()
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ds.slab.launches()
+    red_dev = "cuda" if args.backend == "nccl" else "cpu"
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         dist.barrier()
@@ -305,33 +334,42 @@ def bench_multi(args):
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1)], device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    launches = torch.tensor([ds.slab.launches() - l0], device="cuda", dtype=torch.int64)
+    launches = torch.tensor([ds.slab.launches() - l0], device=red_dev, dtype=torch.int64)
     dist.all_reduce(launches)
     ms = float(ms.item())
     value = nvox * args.steps / (ms / 1e3)
+    ds.slab.close()
 
-    # e2e: host inputs -> slabs (H2D) -> ITERS_CFG steps -> D2H of owned planes, max over ranks
+    # e2e: this rank's host planes -> device (H2D), init, ITERS_CFG steps, D2H of
+    # the owned planes; wall clock, max over ranks.
     e2e_t = []
     for i in range(1 + args.e2e_steps):
         dist.barrier()
         t0 = time.perf_counter()
-        d2 = DistSlab(phi0, img, p, fields=args.fields)
+        d2 = DistSlab(h_phi, h_img, p, fields=args.fields, transport=transport)
         for _ in range(ITERS_CFG):
             d2.step()
         _ = d2.phi_owned()
         d2.slab.close()
-        t = torch.tensor([time.perf_counter() - t0], device="cuda")
+        t = torch.tensor([time.perf_counter() - t0], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if i > 0:
             e2e_t.append(float(t.item()))
     if rank == 0:
+        cfg = workload_config(world, args.fields)
+        cfg.update({"workload": f"weak scaling: 512x512x{nz_total} tube network (cfg2 density, "
+                                f"{spec['n_branches']} branches), one 512^3 z-slab per GPU, sigma1=3 (R=9), "
+                                "3d-paper params, phi0 = threshold init",
+                    "nz": nz_total, "decomposition": f"z-slabs x{world}, halo R=9 planes each way per step "
+                                                     f"({args.backend}, overlapped with the owned planes' xy work)",
+                    "l2": "inputs larger than L2; no flush"})
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-               "data": "synthetic (reference phantom spec, seeded)", "config": workload_config(world, args.fields),
-               "e2e": {"value": nvox * ITERS_CFG / statistics.median(e2e_t), "unit": UNIT,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (reference phantom spec, seeded; device generator)", "config": cfg,
+               "e2e": {"value": nvox * ITERS_CFG / statistics.median(e2e_t) if e2e_t else None, "unit": UNIT,
                        "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
                        "iterations_per_step": ITERS_CFG, "api": "spmd.DistSlab (host buffers)"},
                "gpu_launches": int(launches.item()), "clocks": clk.summary(), "roofline": None,
@@ -356,7 +394,7 @@ def bench_reference(args):
     sample = f"{args.steps} timed evolve_step (after {args.warmup} warm-up) on planes [0,{planes}) of the 512^3 volume"
     out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (reference)",
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (reference)",
            "data": "synthetic (reference phantom spec, seeded)", "config": workload_config(1, 4),
            "impl": "reference",
            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
@@ -374,6 +412,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-planes", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="N > 1 halo transport")
+    ap.add_argument("--share-gpu", action="store_true", help="N > 1 ranks all on cuda:0 (testing; gloo)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

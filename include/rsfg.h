@@ -162,6 +162,8 @@ int rsfg_slab_create(rsfg_slab** out, int32_t nx, int32_t ny, int32_t nz, int32_
 int rsfg_slab_geometry(const rsfg_slab* s, int32_t* zb, int32_t* ze, int32_t* halo);
 /* Host planes [zb, ze) of phi0 and I. */
 int rsfg_slab_upload(rsfg_slab* s, const float* phi_held, const float* image_held);
+/* Same from DEVICE pointers (the held planes, on the slab's device). */
+int rsfg_slab_upload_device(rsfg_slab* s, const float* d_phi_held, const float* d_image_held);
 /* min/max of I over the owned planes; the caller reduces across slabs and
  * passes the global pair to rsfg_slab_init (volume.cpp:25-33 semantics). */
 int rsfg_slab_local_range(rsfg_slab* s, float* i_min, float* i_max);

@@ -141,6 +141,7 @@ SIGNATURES = {
     "rsfg_slab_create": (C.c_int, [P(VP), I32, I32, I32, I32, I32, P(rsfg_params), P(rsfg_options)]),
     "rsfg_slab_geometry": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
     "rsfg_slab_upload": (C.c_int, [VP, FP, FP]),
+    "rsfg_slab_upload_device": (C.c_int, [VP, FP, FP]),
     "rsfg_slab_local_range": (C.c_int, [VP, P(C.c_float), P(C.c_float)]),
     "rsfg_slab_init": (C.c_int, [VP, C.c_float, C.c_float]),
     "rsfg_slab_halo": (C.c_int, [VP, I32, P(VP), P(VP), P(C.c_int64)]),

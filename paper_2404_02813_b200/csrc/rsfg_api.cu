@@ -971,6 +971,13 @@ __attribute__((visibility("default"))) int rsfg_slab_upload(rsfg_slab* s, const 
   return RSFG_OK;
 }
 
+__attribute__((visibility("default"))) int rsfg_slab_upload_device(rsfg_slab* s, const float* phi, const float* image) {
+  if (!s || !phi || !image) return fail(RSFG_ERR_STATE, "null argument");
+  if (int rc = upload(s, phi, image, cudaMemcpyDeviceToDevice)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return RSFG_OK;
+}
+
 __attribute__((visibility("default"))) int rsfg_slab_local_range(rsfg_slab* s, float* lo, float* hi) {
   if (!s || !lo || !hi) return fail(RSFG_ERR_STATE, "null argument");
   return local_range(s, lo, hi);

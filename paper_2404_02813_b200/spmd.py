@@ -59,8 +59,14 @@ class Slab:
         check(self.lib.rsfg_slab_geometry(self.h, C.byref(zb), C.byref(ze), C.byref(halo)))
         self.zb, self.ze, self.halo = zb.value, ze.value, halo.value
 
-    def upload(self, phi_vol: np.ndarray, img_vol: np.ndarray):
-        """Takes the FULL volumes and uploads the held planes [zb, ze)."""
+    def upload(self, phi_vol, img_vol):
+        """Takes the FULL volumes (numpy host arrays, or torch CUDA tensors on
+        the slab's device) and uploads the held planes [zb, ze)."""
+        if hasattr(phi_vol, "data_ptr"):  # torch CUDA tensors: device-to-device
+            ph = phi_vol[self.zb:self.ze].contiguous()
+            im = img_vol[self.zb:self.ze].contiguous()
+            check(self.lib.rsfg_slab_upload_device(self.h, ph.data_ptr(), im.data_ptr()))
+            return
         ph = np.ascontiguousarray(phi_vol[self.zb:self.ze], np.float32)
         im = np.ascontiguousarray(img_vol[self.zb:self.ze], np.float32)
         check(self.lib.rsfg_slab_upload(self.h, ph.ctypes.data, im.ctypes.data))
