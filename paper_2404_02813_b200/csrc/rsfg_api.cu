@@ -221,10 +221,11 @@ void make_xy2_maps(rsfg_slab* s) {
   const char* off = std::getenv("RSFG_XY2");
   if ((off && off[0] == '0') || !s->fast || (s->nx % 4) != 0) return;
   // Tile height: 64 x 64 (1 CTA/SM, 16 warps) amortises the Heaviside halo
-  // better at large radii; 64 x 32 (2 CTAs/SM) wins up to R = 12
+  // better at large radii (fields=2; the fields=4 64 x 64 tile does not fit
+  // shared memory); 64 x 32 (2 CTAs/SM) wins up to R = 12
   // (profiles/r01_xy2_tile_height.txt).  RSFG_XY2_TY=32|64 overrides.
   const char* ty = std::getenv("RSFG_XY2_TY");
-  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 ? 64 : 32);
+  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 && s->fields == 2 ? 64 : 32);
   int bx = 0, by = 0;
   if (!rsfg::xy2_box(s->t1.r, s->xy2_ty, &bx, &by)) return;
   const int planes = s->ze - s->zb;
@@ -243,21 +244,21 @@ void make_z_maps(rsfg_slab* s) {
   s->zmaps[0].valid = s->zmaps[1].valid = false;
   const char* off = std::getenv("RSFG_ZST4");
   if ((off && off[0] == '0') || !s->fast || (s->nx % 4) != 0) return;
-  int bz = 0;
-  if (!rsfg::zst4_box(s->t1.r, s->fields, &bz)) return;
+  int bz = 0, ty = 8;
+  if (!rsfg::zst4_box(s->t1.r, s->fields, &bz, &ty)) return;
   const int planes = s->ze - s->zb;
   // A P window deeper than the held planes is never loaded by TMA (the
   // kernel's in-range test fails for every group); encode a valid map anyway.
   rsfg::ZMaps m;
   for (int f = 0; f < 2; ++f) {
     const float2* P = s->P[f] ? s->P[f] : s->P[0];
-    if (!encode_map(&m.p[f], P, 2 * s->nx, s->ny, planes, 64, 8, std::min(bz, planes))) return;
+    if (!encode_map(&m.p[f], P, 2 * s->nx, s->ny, planes, 64, ty, std::min(bz, planes))) return;
   }
-  if (!encode_map(&m.ki, s->ki, s->nx, s->ny, planes, 32, 8, 1)) return;
-  if (!encode_map(&m.k1i, s->k1i ? s->k1i : s->ki, s->nx, s->ny, planes, 32, 8, 1)) return;
+  if (!encode_map(&m.ki, s->ki, s->nx, s->ny, planes, 32, ty, 1)) return;
+  if (!encode_map(&m.k1i, s->k1i ? s->k1i : s->ki, s->nx, s->ny, planes, 32, ty, 1)) return;
   for (int b = 0; b < 2; ++b) {
     s->zmaps[b] = m;
-    if (!encode_map(&s->zmaps[b].phi, s->phi[b], s->nx, s->ny, planes, 40, 12, 1)) return;
+    if (!encode_map(&s->zmaps[b].phi, s->phi[b], s->nx, s->ny, planes, 40, ty + 4, 1)) return;
   }
   s->zmaps[0].valid = s->zmaps[1].valid = true;
 }

@@ -67,8 +67,8 @@ struct XYMaps {
 };
 
 // TMA descriptors of kernel 2's (zst4) inputs for one phi buffer: the phi
-// plane ring box (40 x 12 x 1 floats), the static fields and the P pair windows (P viewed as
-// 2*nx floats per row, box 64 x 8 x (8 + 2R)).  valid == false -> zst kernel.
+// plane ring box (40 x (TY+4) x 1 floats), the static fields (32 x TY) and
+// the P pair windows (P viewed as 2*nx floats per row, box 64 x TY x (8 + 2R)).  valid == false -> zst kernel.
 struct ZMaps {
   CUtensorMap phi;
   CUtensorMap ki, k1i;  // K2*I (== I for sigma2 = 0) and K1*I, box 32 x 8 x 1
@@ -76,9 +76,10 @@ struct ZMaps {
   bool valid;
 };
 
-// Window depth (planes) of zst4's P box for radius r; false if zst4 has no
-// specialisation for (r, fields) or it does not fit shared memory.
-bool zst4_box(int r, int fields, int* pbox_z);
+// Window depth (planes) of zst4's P box and its column-tile height (8, or 4
+// for large radii) for radius r; false if zst4 has no specialisation for
+// (r, fields) or it does not fit shared memory.
+bool zst4_box(int r, int fields, int* pbox_z, int* ty);
 
 // Kernel 2, TMA-fed variant (update mode only).  -1 when not applicable.
 int launch_zst4(const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b, int z_begin,

@@ -4,10 +4,10 @@
 
 namespace rsfg {
 
-bool zst4_box(int r, int fields, int* pbox_z) {
+bool zst4_box(int r, int fields, int* pbox_z, int* ty) {
   int rc = -2;
 #define TRY(N) \
-  if (rc == -2) rc = zst4_group_box_##N(r, fields, pbox_z);
+  if (rc == -2) rc = zst4_group_box_##N(r, fields, pbox_z, ty);
   RSFG_ZST4_GROUPS(TRY)
 #undef TRY
   return rc == 1;

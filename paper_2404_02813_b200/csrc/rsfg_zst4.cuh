@@ -34,12 +34,15 @@ namespace {
 
 template <int R, int NP>
 struct Z4 {
-  static constexpr int TX = 32, TY = 8, NT = TX * TY;
-  static constexpr int BX = 40, BY = 12, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
+  // 32 x 8 columns; 32 x 4 for large radii, whose z-pass window (8 + 2R
+  // planes of P) would otherwise leave one CTA per SM.
+  static constexpr int TX = 32, TY = R >= 17 ? 4 : 8, NT = TX * TY;
+  static constexpr int kMinBlocks = TY == 4 && NP == 1 ? 3 : 2;  // CTAs per SM the registers must allow
+  static constexpr int BX = 40, BY = TY + 4, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
   static constexpr int kProducer = 3 * 32;                // TMA-issuing thread (warp 3, no halo work)
-  static_assert(kHalo > 2 * 32 && kHalo <= 2 * 32 + 16, "halo slots: warps 0, 1 and half of warp 2");
+  static_assert(kHalo > 2 * 32 && kHalo <= 3 * 32 && NT >= 4 * 32, "halo slots: warps 0, 1 and part of warp 2");
   static constexpr int G = 8;                             // planes per group (z-pass chunk, ring period)
   static constexpr int TZ = 128;                          // planes per CTA
   static constexpr int NW = G + 2 * R;                    // z-pass window (planes)
@@ -102,13 +105,13 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   // lanes 0..15); the TMA producer is warp 3 (kProducer), so no warp carries
   // two of the extra jobs into the per-plane barrier.
   // Warps 0..2 all take the halo branch (warp-uniform: no reconvergence
-  // bookkeeping); warp 2's lanes 16..31 repeat lanes 0..15 (same values to the
-  // same addresses).
+  // bookkeeping); warp 2's lanes past the last halo slot repeat its first
+  // ones (same values to the same addresses).
   const bool has_halo = __any_sync(0xffffffffu, tid < C::kHalo);
   NPos hal = own;
   if (has_halo) {
     int i, j;
-    const int h = tid < C::kHalo ? tid : tid - 16;
+    const int h = tid < C::kHalo ? tid : 2 * C::TX + (tid - 2 * C::TX) % (C::kHalo - 2 * C::TX);
     if (h < C::TX) {
       i = h + 1, j = 0;
     } else if (h < 2 * C::TX) {
@@ -380,7 +383,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
 }
 
 template <int R, int NP>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(Z4<R, NP>::NT, Z4<R, NP>::kMinBlocks)
     zst4_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end,
                 const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_ki,
                 const __grid_constant__ CUtensorMap map_k1i, const __grid_constant__ CUtensorMap map_p0,
@@ -433,7 +436,7 @@ int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuf
 #define RSFG_ZST4_DECL(N)                                                                              \
   int zst4_group_##N(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c,             \
                      const StepBuffers& b, int z_begin, int z_end, const ZMaps& m, cudaStream_t st);    \
-  int zst4_group_box_##N(int r, int fields, int* pbox_z);
+  int zst4_group_box_##N(int r, int fields, int* pbox_z, int* ty);
 RSFG_ZST4_GROUPS(RSFG_ZST4_DECL)
 #undef RSFG_ZST4_DECL
 

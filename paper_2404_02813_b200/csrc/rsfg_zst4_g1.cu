@@ -4,19 +4,23 @@
 
 namespace rsfg {
 
-int zst4_group_box_1(int r, int fields, int* pbox_z) {
+int zst4_group_box_1(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 4:
       *pbox_z = Z4<4, 1>::NW;
+      *ty = Z4<4, 1>::TY;
       return (fields == 4 ? Z4<4, 2>::kSmem : Z4<4, 1>::kSmem) <= 227 * 1024;
     case 5:
       *pbox_z = Z4<5, 1>::NW;
+      *ty = Z4<5, 1>::TY;
       return (fields == 4 ? Z4<5, 2>::kSmem : Z4<5, 1>::kSmem) <= 227 * 1024;
     case 6:
       *pbox_z = Z4<6, 1>::NW;
+      *ty = Z4<6, 1>::TY;
       return (fields == 4 ? Z4<6, 2>::kSmem : Z4<6, 1>::kSmem) <= 227 * 1024;
     case 7:
       *pbox_z = Z4<7, 1>::NW;
+      *ty = Z4<7, 1>::TY;
       return (fields == 4 ? Z4<7, 2>::kSmem : Z4<7, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -4,13 +4,15 @@
 
 namespace rsfg {
 
-int zst4_group_box_2(int r, int fields, int* pbox_z) {
+int zst4_group_box_2(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 8:
       *pbox_z = Z4<8, 1>::NW;
+      *ty = Z4<8, 1>::TY;
       return (fields == 4 ? Z4<8, 2>::kSmem : Z4<8, 1>::kSmem) <= 227 * 1024;
     case 9:
       *pbox_z = Z4<9, 1>::NW;
+      *ty = Z4<9, 1>::TY;
       return (fields == 4 ? Z4<9, 2>::kSmem : Z4<9, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -4,13 +4,15 @@
 
 namespace rsfg {
 
-int zst4_group_box_3(int r, int fields, int* pbox_z) {
+int zst4_group_box_3(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 10:
       *pbox_z = Z4<10, 1>::NW;
+      *ty = Z4<10, 1>::TY;
       return (fields == 4 ? Z4<10, 2>::kSmem : Z4<10, 1>::kSmem) <= 227 * 1024;
     case 11:
       *pbox_z = Z4<11, 1>::NW;
+      *ty = Z4<11, 1>::TY;
       return (fields == 4 ? Z4<11, 2>::kSmem : Z4<11, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -4,10 +4,11 @@
 
 namespace rsfg {
 
-int zst4_group_box_5(int r, int fields, int* pbox_z) {
+int zst4_group_box_5(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 18:
       *pbox_z = Z4<18, 1>::NW;
+      *ty = Z4<18, 1>::TY;
       return (fields == 4 ? Z4<18, 2>::kSmem : Z4<18, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
