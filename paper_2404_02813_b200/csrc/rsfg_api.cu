@@ -119,6 +119,12 @@ struct rsfg_slab {
   rsfg::ZMaps zmaps[2] = {};                // TMA maps for kernel 2 (zst4), per phi buffer
   rsfg::XYMaps xy2maps[2] = {};             // TMA maps for kernel 1 (xy2), per phi buffer
   int xy2_ty = 32;                          // xy2 tile height
+  // Stored-Heaviside mode (fields=2, sigma2=0, zst4 + xy2): kernel 2 writes
+  // (H-, H- I) of phi' and kernel 1 reads it.  hh_valid: the owned planes'
+  // pairs match the current phi (halo planes are always recomputed).
+  float2* hh = nullptr;
+  bool hh_mode = false;
+  bool hh_valid = false;
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -161,6 +167,7 @@ void release(rsfg_slab* s) {
   cudaFree(s->P[0]);
   cudaFree(s->P[1]);
   cudaFree(s->scratch);
+  cudaFree(s->hh);
   cudaFree(s->counters);
   cudaFree(s->mm);
   if (s->h_counters) cudaFreeHost(s->h_counters);
@@ -236,6 +243,20 @@ void make_xy2_maps(rsfg_slab* s) {
     s->xy2maps[b].img = img;
   }
   s->xy2maps[0].valid = s->xy2maps[1].valid = true;
+  // Stored-Heaviside mode: kernel 2 evaluates H once per voxel instead of
+  // kernel 1 on every haloed tile.  It pays while the Heaviside is a large
+  // share of kernel 1 (R <= 9: step -7 % at sigma 3; at R = 12 kernel 2's
+  // extra work cancels the gain, profiles/r01_hh_mode.txt).  RSFG_HH=0|1
+  // overrides.  Needs zst4 (it writes the pairs).
+  const char* hh_env = std::getenv("RSFG_HH");
+  const bool hh_want = hh_env ? hh_env[0] == '1' : s->t1.r <= 9;
+  if (hh_want && s->xy2_ty == 32 && s->fields == 2 && s->t2.r == 0 && s->zmaps[0].valid && s->hh) {
+    CUtensorMap m;
+    if (encode_map(&m, s->hh, 2 * s->nx, s->ny, planes, 2 * bx, by, 1)) {
+      for (int b = 0; b < 2; ++b) s->xy2maps[b].hh = m, s->xy2maps[b].use_hh = true;
+      s->hh_mode = true;
+    }
+  }
 }
 
 // TMA descriptors for kernel 2 (zst4).  Needs nx % 4 == 0 (16-byte phi rows).
@@ -327,6 +348,8 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
+  if (s->fast && s->fields == 2 && s->t2.r == 0 && (s->nx % 4) == 0)
+    CUDA_TRY(cudaMalloc(&s->hh, held * sizeof(float2)));
   make_xy_maps(s);
   make_z_maps(s);
   make_xy2_maps(s);
@@ -357,11 +380,13 @@ int reconfigure(rsfg_slab* s, const rsfg_params* p, const rsfg_options* o) {
   s->iteration = 0;
   s->valid = true;
   s->initialized = false;
+  s->hh_valid = false;
   return RSFG_OK;
 }
 
 int upload(rsfg_slab* s, const float* phi, const float* image, cudaMemcpyKind kind) {
   CUDA_TRY(cudaSetDevice(s->dev));
+  s->hh_valid = false;
   const size_t bytes = s->held() * sizeof(float);
   CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, bytes, kind, s->stream));
   CUDA_TRY(cudaMemcpyAsync(s->image, image, bytes, kind, s->stream));
@@ -424,6 +449,7 @@ rsfg::StepBuffers buffers(rsfg_slab* s, float* out) {
   b.P[1] = s->P[1];
   b.out = out;
   b.counters = s->counters + 2 * s->slot;
+  b.hh = nullptr;
   return b;
 }
 
@@ -433,6 +459,10 @@ int xy_planes(rsfg_slab* s, int a, int b) {
   const rsfg::Geom g = s->geom();
   int n;
   if (s->fast) {
+    if (s->hh_mode && !(s->hh_valid && a >= s->z0 && b <= s->z1)) {
+      // pairs of planes kernel 2 did not write for the current phi
+      s->launches += rsfg::launch_hh(g, s->c.inv_eps, s->phi[s->cur], s->image, s->hh, a, b, s->stream);
+    }
     n = rsfg::launch_xy2(g, s->fields, s->xy2_ty, s->t1, s->c.inv_eps, s->P[0], s->P[1], a, b, s->xy2maps[s->cur],
                          s->stream);
     if (n < 0)
@@ -472,8 +502,12 @@ int step_finish(rsfg_slab* s, rsfg::StepMode mode, float* out) {
   int n;
   if (s->fast) {
     n = -1;
-    if (mode == rsfg::kUpdate)
+    if (mode == rsfg::kUpdate) {
+      b.hh = s->hh_mode ? s->hh : nullptr;
       n = rsfg::launch_zst4(g, s->fields, s->t1, s->c, b, s->z0, s->z1, s->zmaps[s->cur], s->stream);
+      // the pairs now describe phi' (owned planes) iff zst4 ran and wrote them
+      if (s->hh_mode) s->hh_valid = n >= 0;
+    }
     if (n < 0) n = rsfg::launch_zst(g, s->fields, s->t1, s->c, b, s->z0, s->z1, mode, s->stream);
   } else {
     int m = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
@@ -607,6 +641,7 @@ __attribute__((visibility("default"))) int rsfg_state_step(rsfg_state* st, doubl
   if (rc == RSFG_ERR_BLOWUP) {
     // rsf.cpp:346-353 throws before the swap: phi and iteration unchanged.
     s->cur ^= 1;
+    s->hh_valid = false;
     s->iteration -= 1;
     s->slot = (s->slot + kSlots - 1) % kSlots;
     return rc;
@@ -710,6 +745,7 @@ __attribute__((visibility("default"))) int rsfg_state_write_phi(rsfg_state* st, 
   CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, s->held() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->valid = true;
+  s->hh_valid = false;
   return RSFG_OK;
 }
 

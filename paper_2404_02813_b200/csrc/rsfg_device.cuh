@@ -79,6 +79,59 @@ __device__ __forceinline__ void heaviside_pair(float phi, float inv_eps, float& 
   hp = 0.5f + sA;
 }
 
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; add.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mul.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 a,b,c,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mov.b64 c,{%6,%7}; fma.rn.f32x2 d,a,b,c; "
+      "mov.b64 {%0,%1},d;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
+
+// Heaviside pair of two voxels, packed: hm = H-(phi), hp = H+(phi) with
+// H+ = 1/2 [1 + (2/pi) atan(phi/eps)] (rsf.cpp:22-25, 89-90).  Same
+// evaluation as heaviside_pair (rsfg_device.cuh), bit for bit: atan(q)/pi on
+// q = min(t, 1/t) in [0, 1].
+template <bool WANT_HP>
+__device__ __forceinline__ void heaviside2(float2 phi, float inv_eps, float2& hm, float2& hp) {
+  const float2 u = f2mul(phi, f2s(inv_eps));
+  const float tx = fabsf(u.x), ty = fabsf(u.y);
+  const float2 q = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
+  const float2 x = f2mul(q, q);
+  float2 p = f2fma(f2s(0.000906360219232738f), x, f2s(-0.00511184660717845f));
+  p = f2fma(p, x, f2s(0.013584661297500134f));
+  p = f2fma(p, x, f2s(-0.023883428424596786f));
+  p = f2fma(p, x, f2s(0.0338696613907814f));
+  p = f2fma(p, x, f2s(-0.04521126672625542f));
+  p = f2fma(p, x, f2s(0.06363844871520996f));
+  p = f2fma(p, x, f2s(-0.10610246658325195f));
+  p = f2fma(p, x, f2s(0.31830987334251404f));
+  const float2 a = f2mul(p, q);  // atan(q)/pi in [0, 1/4]
+  // A = atan(t)/pi = far ? 1/2 - a : a; H- = 1/2 - sign(u) A, H+ = 1/2 + sign(u) A.
+  // On the far side the small H is 1/2 - (1/2 - a): exact but for one rounding
+  // of 1/2 - a (3e-8 absolute), where delta(phi) <= 1/(pi t^2) is negligible.
+  const float2 am = f2add(f2s(0.5f), make_float2(-a.x, -a.y));
+  const float2 A = make_float2(tx > 1.0f ? am.x : a.x, ty > 1.0f ? am.y : a.y);
+  const float2 sA = make_float2(copysignf(A.x, u.x), copysignf(A.y, u.y));
+  hm = f2add(f2s(0.5f), make_float2(-sA.x, -sA.y));
+  if constexpr (WANT_HP) hp = f2add(f2s(0.5f), sA);
+}
+
 // ---- TMA (cp.async.bulk.tensor) + mbarrier, sm_90+/sm_100a PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

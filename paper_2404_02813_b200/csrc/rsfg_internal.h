@@ -51,6 +51,7 @@ struct StepBuffers {
   float2* P[2];
   float* out;                       // phi_{n+1} (mode 0) or E (mode 1)
   unsigned long long* counters;     // [0] sign changes, [1] first bad index (min)
+  float2* hh;                       // zst4, fields=2, sigma2=0: (H-, H- I) of phi_{n+1}, or null
 };
 
 enum StepMode { kUpdate = 0, kEnergy = 1 };
@@ -64,6 +65,8 @@ struct XYMaps {
   CUtensorMap phi;
   CUtensorMap img;
   bool valid;
+  CUtensorMap hh;  // stored-Heaviside mode (xy2 only): (H-, H- I) pairs, box 2*BOXX x WY floats
+  bool use_hh;
 };
 
 // TMA descriptors of kernel 2's (zst4) inputs for one phi buffer: the phi
@@ -127,6 +130,11 @@ float decode_ordered(unsigned int u);
 unsigned int encode_ordered(float f);
 
 int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st);
+
+// (H-, H- I) of phi for planes [z_begin, z_end) (the pairs kernel 1 reads in
+// the stored-Heaviside mode); same bits as zst4's in-kernel evaluation.
+int launch_hh(const Geom& g, float inv_eps, const float* phi, const float* image, float2* hh, int z_begin,
+              int z_end, cudaStream_t st);
 
 // Sets the calling thread's rsfg_last_error() message (rsfg_api.cu).
 void set_error(const std::string& msg);

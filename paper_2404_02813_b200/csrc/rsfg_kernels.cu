@@ -162,6 +162,24 @@ float decode_ordered(unsigned int u) {
   return f;
 }
 
+__global__ void hh_kernel(Geom g, float inv_eps, const float* __restrict__ phi, const float* __restrict__ image,
+                          float2* __restrict__ hh, long long first, long long n) {
+  for (long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < first + n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float hm, hp;
+    heaviside_pair(phi[i], inv_eps, hm, hp);
+    hh[i] = make_float2(hm, hm * image[i]);
+  }
+}
+
+int launch_hh(const Geom& g, float inv_eps, const float* phi, const float* image, float2* hh, int z_begin,
+              int z_end, cudaStream_t st) {
+  if (z_end <= z_begin) return 0;
+  const long long n = (long long)(z_end - z_begin) * g.plane;
+  hh_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, inv_eps, phi, image, hh, (long long)(z_begin - g.zb) * g.plane, n);
+  return 1;
+}
+
 int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st) {
   mask_kernel<<<grid_for(n, 256), 256, 0, st>>>(phi, mask, n);
   return 1;

@@ -23,59 +23,6 @@
 namespace rsfg {
 namespace {
 
-__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; add.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mul.rn.f32x2 d,a,b; mov.b64 {%0,%1},d;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{.reg .b64 a,b,c,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mov.b64 c,{%6,%7}; fma.rn.f32x2 d,a,b,c; "
-      "mov.b64 {%0,%1},d;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
-
-// Heaviside pair of two voxels, packed: hm = H-(phi), hp = H+(phi) with
-// H+ = 1/2 [1 + (2/pi) atan(phi/eps)] (rsf.cpp:22-25, 89-90).  Same
-// evaluation as heaviside_pair (rsfg_device.cuh), bit for bit: atan(q)/pi on
-// q = min(t, 1/t) in [0, 1].
-template <bool WANT_HP>
-__device__ __forceinline__ void heaviside2(float2 phi, float inv_eps, float2& hm, float2& hp) {
-  const float2 u = f2mul(phi, f2s(inv_eps));
-  const float tx = fabsf(u.x), ty = fabsf(u.y);
-  const float2 q = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
-  const float2 x = f2mul(q, q);
-  float2 p = f2fma(f2s(0.000906360219232738f), x, f2s(-0.00511184660717845f));
-  p = f2fma(p, x, f2s(0.013584661297500134f));
-  p = f2fma(p, x, f2s(-0.023883428424596786f));
-  p = f2fma(p, x, f2s(0.0338696613907814f));
-  p = f2fma(p, x, f2s(-0.04521126672625542f));
-  p = f2fma(p, x, f2s(0.06363844871520996f));
-  p = f2fma(p, x, f2s(-0.10610246658325195f));
-  p = f2fma(p, x, f2s(0.31830987334251404f));
-  const float2 a = f2mul(p, q);  // atan(q)/pi in [0, 1/4]
-  // A = atan(t)/pi = far ? 1/2 - a : a; H- = 1/2 - sign(u) A, H+ = 1/2 + sign(u) A.
-  // On the far side the small H is 1/2 - (1/2 - a): exact but for one rounding
-  // of 1/2 - a (3e-8 absolute), where delta(phi) <= 1/(pi t^2) is negligible.
-  const float2 am = f2add(f2s(0.5f), make_float2(-a.x, -a.y));
-  const float2 A = make_float2(tx > 1.0f ? am.x : a.x, ty > 1.0f ? am.y : a.y);
-  const float2 sA = make_float2(copysignf(A.x, u.x), copysignf(A.y, u.y));
-  hm = f2add(f2s(0.5f), make_float2(-sA.x, -sA.y));
-  if constexpr (WANT_HP) hp = f2add(f2s(0.5f), sA);
-}
-
 template <int R, int NP, int TY>
 struct XY2 {
   static constexpr int TX = 64;
@@ -107,6 +54,9 @@ struct XY2 {
   static constexpr bool kOsAlias = kHsBytes + kYsBytes + kOsBytes + 2 * kTile + 16 > 112 * 1024 &&
                                    kOsBytes <= kHsBytes;
   static constexpr size_t kSmem = kHsBytes + kYsBytes + (kOsAlias ? 0 : kOsBytes) + 2 * kTile + 16;
+  // stored-Heaviside variant (xy2_cta_hh): two (H-, H- I) tile buffers, Ys, Os
+  static constexpr size_t kTileHH = ((size_t)BOXX * WY * sizeof(float2) + 127) & ~(size_t)127;
+  static constexpr size_t kSmemHH = 2 * kTileHH + kYsBytes + kOsBytes + 16;
   static constexpr int RG = NT / NPR;                     // row groups of phase A
   static constexpr int RITER = (WY + RG - 1) / RG;        // rows per phase-A thread
   static constexpr int YIT = (NP * WX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
@@ -329,6 +279,163 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
   }
 }
 
+// Stored-Heaviside variant (fields=2, sigma2 = 0): kernel 2 of the previous
+// step wrote (H-, H- I) of phi, so the tile arrives ready for the y pass --
+// no Heaviside phase and no halo recomputation.  Two tile buffers: plane z+1
+// is requested as soon as plane z's wait returns (its buffer held plane z-1,
+// whose y pass ended two barriers earlier).
+template <int R, int TY, bool EDGE>
+__device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, float2* __restrict__ P0, int z_first,
+                                           int z_last, int x0, int y0, const CUtensorMap* map_hh,
+                                           unsigned char* smem) {
+  using C = XY2<R, 1, TY>;
+  float2* __restrict__ Ys = reinterpret_cast<float2*>(smem + 2 * C::kTileHH);                 // [TY][PY]
+  float2* __restrict__ Os = reinterpret_cast<float2*>(smem + 2 * C::kTileHH + C::kYsBytes);  // [TY][PO]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kSmemHH - 16);
+  const int tid = threadIdx.x;
+  const int bx0 = x0 - R - C::SHIFT, by0 = y0 - R;
+
+  int ysrc[C::YIT], ydst[C::YIT];
+  constexpr int SEGY = TY / C::BY;
+#pragma unroll
+  for (int i = 0; i < C::YIT; ++i) {
+    const int it = min(tid + i * C::NT, C::WX * SEGY - 1);
+    const int sy = it / C::WX, cx = it - sy * C::WX;
+    ysrc[i] = (sy * C::BY) * C::BOXX + C::SHIFT + cx;
+    ydst[i] = (sy * C::BY) * C::PY + cx;
+  }
+  const bool y_last = tid + (C::YIT - 1) * C::NT < C::WX * SEGY;
+  int xsrc[C::XIT], xdst[C::XIT];
+  constexpr int SEGX = C::TX / C::BX;
+#pragma unroll
+  for (int i = 0; i < C::XIT; ++i) {
+    const int it = min(tid + i * C::NT, TY * SEGX - 1);
+    const int sx = it / TY, row = it - sx * TY;
+    xsrc[i] = row * C::PY + sx * C::BX;
+    xdst[i] = row * C::PO + sx * C::BX;
+  }
+  const bool x_last = tid + (C::XIT - 1) * C::NT < TY * SEGX;
+  int osrc[C::OIT];
+  size_t odst[C::OIT];
+  bool o_ok[C::OIT];
+#pragma unroll
+  for (int i = 0; i < C::OIT; ++i) {
+    const int it = min(tid + i * C::NT, TY * C::TX / 2 - 1);
+    const int row = it / (C::TX / 2), cp = it - row * (C::TX / 2);
+    osrc[i] = row * C::PO + 2 * cp;
+    const int gx = x0 + 2 * cp, gy = y0 + row;
+    o_ok[i] = tid + i * C::NT < TY * C::TX / 2 && (!EDGE || (gx < g.nx && gy < g.ny));
+    odst[i] = (size_t)min(gy, g.ny - 1) * g.nx + min(gx, g.nx - 2);
+  }
+
+  auto issue = [&](int z, int buf) {
+    mbar_expect_tx(bars + buf, (uint32_t)(C::BOXX * C::WY * sizeof(float2)));
+    tma_load_3d(smem + buf * C::kTileHH, map_hh, bars + buf, 2 * bx0, by0, z - g.zb);
+  };
+  if (tid == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    issue(z_first, 0);
+  }
+  __syncthreads();
+
+#pragma unroll 1
+  for (int z = z_first; z < z_last; ++z) {
+    const int xb = (z - z_first) & 1;
+    float2* T = reinterpret_cast<float2*>(smem + xb * C::kTileHH);  // [WY][BOXX] (H-, H- I)
+    mbar_wait(bars + xb, (uint32_t)(((z - z_first) >> 1) & 1));
+    if (tid == 0 && z + 1 < z_last) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(z + 1, xb ^ 1);
+    }
+    if constexpr (EDGE) {  // clamp-to-edge fix-up of the pairs outside the volume
+      const int lo = max(0, -bx0), hi = min(C::BOXX, g.nx - bx0);
+      const int nfix = lo + (C::BOXX - hi);
+      for (int e = tid; e < C::WY * nfix; e += C::NT) {
+        const int ry = e / nfix, k = e - ry * nfix;
+        const int cdst = k < lo ? k : hi + (k - lo);
+        const int csrc = k < lo ? lo : hi - 1;
+        T[ry * C::BOXX + cdst] = T[ry * C::BOXX + csrc];
+      }
+      __syncthreads();
+      const int ylo = max(0, -by0), yhi = min(C::WY, g.ny - by0);
+      const int nrow = ylo + (C::WY - yhi);
+      for (int e = tid; e < nrow * C::BOXX; e += C::NT) {
+        const int k = e / C::BOXX, cx = e - k * C::BOXX;
+        const int rdst = k < ylo ? k : yhi + (k - ylo);
+        const int rsrc = k < ylo ? ylo : yhi - 1;
+        T[rdst * C::BOXX + cx] = T[rsrc * C::BOXX + cx];
+      }
+      __syncthreads();
+    }
+    // ---- y pass straight from the tile (lanes walk x: consecutive pairs)
+#pragma unroll
+    for (int i = 0; i < C::YIT; ++i) {
+      if (i < C::YIT - 1 || y_last) {
+        const float2* src = T + ysrc[i];
+        float2 v[C::BY + 2 * R];
+#pragma unroll
+        for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::BOXX];
+        float2* dst = Ys + ydst[i];
+#pragma unroll
+        for (int b = 0; b < C::BY; ++b) {
+          float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+          dst[b * C::PY] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- x pass (lanes walk rows of the odd-pitched Ys) into the staging tile
+#pragma unroll
+    for (int i = 0; i < C::XIT; ++i) {
+      if (i < C::XIT - 1 || x_last) {
+        const float2* src = Ys + xsrc[i];
+        float2 v[C::BX + 2 * R];
+#pragma unroll
+        for (int k = 0; k < C::BX + 2 * R; ++k) v[k] = src[k];
+        float2 o[C::BX];
+#pragma unroll
+        for (int b = 0; b < C::BX; ++b) {
+          float2 acc = fmul2(taps.w[0], v[b]);
+#pragma unroll
+          for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
+          o[b] = acc;
+        }
+        float4* dst = reinterpret_cast<float4*>(Os + xdst[i]);
+#pragma unroll
+        for (int b = 0; b < C::BX / 2; ++b) dst[b] = make_float4(o[2 * b].x, o[2 * b].y, o[2 * b + 1].x, o[2 * b + 1].y);
+      }
+    }
+    __syncthreads();
+    // ---- coalesced 16-byte stores of P
+    float2* Pz = P0 + (size_t)(z - g.zb) * (size_t)g.plane;
+#pragma unroll
+    for (int i = 0; i < C::OIT; ++i)
+      if (o_ok[i]) *reinterpret_cast<float4*>(Pz + odst[i]) = *reinterpret_cast<const float4*>(Os + osrc[i]);
+    // next plane: the y pass rewrites Ys after this plane's x pass (barrier
+    // above); the x pass rewrites Os after the next y-pass barrier, which
+    // every thread reaches after this copy-out.
+  }
+}
+
+template <int R, int TY>
+__global__ void __launch_bounds__(XY2<R, 1, TY>::NT, XY2<R, 1, TY>::NT == 256 ? 2 : 1)
+    xy2_hh_kernel(Geom g, Taps taps, float2* __restrict__ P0, int z_begin, int z_end,
+                  const __grid_constant__ CUtensorMap map_hh) {
+  using C = XY2<R, 1, TY>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int x0 = blockIdx.x * C::TX, y0 = blockIdx.y * TY;
+  const int z_first = z_begin + blockIdx.z * C::NZC;
+  const int z_last = min(z_first + C::NZC, z_end);
+  const bool edge = x0 - R < 0 || y0 - R < 0 || x0 - R + C::WX > g.nx || y0 - R + C::WY > g.ny;
+  if (edge)
+    xy2_cta_hh<R, TY, true>(g, taps, P0, z_first, z_last, x0, y0, &map_hh, smem);
+  else
+    xy2_cta_hh<R, TY, false>(g, taps, P0, z_first, z_last, x0, y0, &map_hh, smem);
+}
+
 template <int R, int NP, int TY>
 __global__ void __launch_bounds__(XY2<R, NP, TY>::NT, XY2<R, NP, TY>::NT == 256 ? 2 : 1)
     xy2_kernel(Geom g, Taps taps, float inv_eps, float2* __restrict__ P0, float2* __restrict__ P1, int z_begin,
@@ -345,9 +452,33 @@ __global__ void __launch_bounds__(XY2<R, NP, TY>::NT, XY2<R, NP, TY>::NT == 256 
     xy2_cta<R, NP, TY, false>(g, taps, inv_eps, P0, P1, z_first, z_last, x0, y0, &map_phi, &map_img, smem);
 }
 
+template <int R, int TY>
+int xy2_hh_launch(const Geom& g, const Taps& t, float2* P0, int z_begin, int z_end, const XYMaps& m,
+                  cudaStream_t st) {
+  using C = XY2<R, 1, TY>;
+  if (C::kSmemHH > 227 * 1024) return -1;
+  auto k = xy2_hh_kernel<R, TY>;
+  static bool attr = false;  // benign race: idempotent attribute set
+  if (!attr) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmemHH) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  if (z_end <= z_begin) return 0;
+  dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
+  k<<<grid, C::NT, C::kSmemHH, st>>>(g, t, P0, z_begin, z_end, m.hh);
+  return 1;
+}
+
 template <int R, int NP, int TY>
 int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* P1, int z_begin, int z_end,
                const XYMaps& m, cudaStream_t st) {
+  // the stored-Heaviside variant exists where the mode is used (R <= 9,
+  // 64 x 32 tiles; rsfg_api.cu make_xy2_maps)
+  if constexpr (NP == 1 && R <= 9 && TY == 32) {
+    if (m.use_hh) return xy2_hh_launch<R, TY>(g, t, P0, z_begin, z_end, m, st);
+  }
+  if (m.use_hh && NP == 1) return -1;
   using C = XY2<R, NP, TY>;
   if (C::kSmem > 227 * 1024) return -1;
   auto k = xy2_kernel<R, NP, TY>;
@@ -368,7 +499,7 @@ int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* 
 // kernel 1 tile height used by xy2 (RSFG_XY2_TY overrides: 32 or 64)
 constexpr int kXY2DefaultTY = 32;
 
-#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3)
+#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6)
 #define RSFG_XY2_DECL(N)                                                                                  \
   int xy2_group_##N(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0,   \
                     float2* P1, int z_begin, int z_end, const XYMaps& m, cudaStream_t st);                 \

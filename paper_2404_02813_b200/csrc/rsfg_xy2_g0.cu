@@ -35,33 +35,28 @@ int xy2_group_0(int r, int ty, const Geom& g, int fields, const Taps& t1, float 
                  int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {
   switch (r) {
     case 0:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<0, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<0, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<0, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<0, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<0, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 1:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<1, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<1, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<1, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<1, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<1, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 2:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<2, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<2, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<2, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<2, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<2, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 3:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<3, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<3, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<3, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<3, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<3, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 4:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<4, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<4, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<4, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<4, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<4, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     default:

@@ -31,27 +31,23 @@ int xy2_group_1(int r, int ty, const Geom& g, int fields, const Taps& t1, float 
                  int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {
   switch (r) {
     case 5:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<5, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<5, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<5, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<5, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<5, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 6:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<6, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<6, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<6, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<6, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<6, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 7:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<7, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<7, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<7, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<7, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<7, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     case 8:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<8, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<8, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<8, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
       return fields == 4 ? xy2_launch<8, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
                          : xy2_launch<8, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     default:

@@ -1,4 +1,4 @@
-// rsfg_xy2_g3.cu -- xy2 (rsfg_xy2.cuh) instantiations for radii [12, 15, 18];
+// rsfg_xy2_g3.cu -- xy2 (rsfg_xy2.cuh) instantiations for radii [10, 11];
 // split across translation units so the build parallelises.
 #include "rsfg_xy2.cuh"
 
@@ -6,17 +6,13 @@ namespace rsfg {
 
 int xy2_group_box_3(int r, int ty, int* bx, int* by) {
   switch (r) {
-    case 12:
-      *bx = ty == 64 ? XY2<12, 1, 64>::BOXX : XY2<12, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<12, 1, 64>::WY : XY2<12, 1, 32>::WY;
+    case 10:
+      *bx = ty == 64 ? XY2<10, 1, 64>::BOXX : XY2<10, 1, 32>::BOXX;
+      *by = ty == 64 ? XY2<10, 1, 64>::WY : XY2<10, 1, 32>::WY;
       return 1;
-    case 15:
-      *bx = ty == 64 ? XY2<15, 1, 64>::BOXX : XY2<15, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<15, 1, 64>::WY : XY2<15, 1, 32>::WY;
-      return 1;
-    case 18:
-      *bx = ty == 64 ? XY2<18, 1, 64>::BOXX : XY2<18, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<18, 1, 64>::WY : XY2<18, 1, 32>::WY;
+    case 11:
+      *bx = ty == 64 ? XY2<11, 1, 64>::BOXX : XY2<11, 1, 32>::BOXX;
+      *by = ty == 64 ? XY2<11, 1, 64>::WY : XY2<11, 1, 32>::WY;
       return 1;
     default:
       return -2;
@@ -26,24 +22,16 @@ int xy2_group_box_3(int r, int ty, int* bx, int* by) {
 int xy2_group_3(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0, float2* P1,
                  int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {
   switch (r) {
-    case 12:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<12, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<12, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<12, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<12, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    case 15:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<15, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<15, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<15, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<15, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    case 18:
-      if (ty == 64)
-        return fields == 4 ? xy2_launch<18, 2, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                           : xy2_launch<18, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<18, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<18, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+    case 10:
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<10, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      return fields == 4 ? xy2_launch<10, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
+                         : xy2_launch<10, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+    case 11:
+      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
+        return fields == 4 ? -1 : xy2_launch<11, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+      return fields == 4 ? xy2_launch<11, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
+                         : xy2_launch<11, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
     default:
       return -2;
   }

@@ -66,7 +66,7 @@ struct NPos {
   float fx, fy;
 };
 
-template <int R, int NP, bool GX>
+template <int R, int NP, bool GX, bool HH>
 __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const StepConsts& c, const StepBuffers& b,
                                          int z0, int z_stop, int x0, int y0, int bx0, int by0,
                                          const CUtensorMap* map_phi, const CUtensorMap* map_ki,
@@ -238,6 +238,8 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
 
     const bool zfast = !GX && zc >= 1 && zc + C::G <= nz - 2 && zc + C::G <= z_stop;
     float* out = b.out + (size_t)(zc - g.zb) * plane + col;
+    float2* hh_out = HH ? b.hh + (size_t)(zc - g.zb) * plane + col : nullptr;
+    float f_prev = 0.0f, ki_prev = 0.0f;  // fast path: Heaviside pairs of planes (q-1, q), packed
 
     auto step = [&](auto kc, auto genc) {
       constexpr int k = decltype(kc)::value;
@@ -275,7 +277,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       }
       const float* K = Kr + ((k + 2) & 7) * C::NK * C::NT + tid;
       const float ki = K[0];
-      const float k1i = NP == 1 ? K[C::NT] : 0.0f;
+      [[maybe_unused]] const float k1i = NP == 1 ? K[C::NT] : 0.0f;
       const float* p1 = Pown + o1;
       float xm1, xp1, ym1, yp1;
       if constexpr (GEN) {
@@ -335,6 +337,26 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
       const float f = fmaf(c.dt_f, e, c0);
       if (!GX || col_ok) {
         out[(size_t)k * plane] = f;
+        if constexpr (HH) {  // stored-Heaviside mode: kernel 1 of the next step reads (H-, H- I) of phi'
+          if constexpr (!GEN) {
+            // full 8-plane group: evaluate planes (q-1, q) as one packed pair
+            // (same bits as the scalar heaviside_pair)
+            if constexpr ((k & 1) == 0) {
+              f_prev = f;
+              ki_prev = ki;
+            } else {
+              float2 hm2, hp2;
+              heaviside2<false>(make_float2(f_prev, f), c.inv_eps, hm2, hp2);
+              const float2 hmi = f2mul(hm2, make_float2(ki_prev, ki));
+              hh_out[(size_t)(k - 1) * plane] = make_float2(hm2.x, hmi.x);
+              hh_out[(size_t)k * plane] = make_float2(hm2.y, hmi.y);
+            }
+          } else {
+            float hm, hp;
+            heaviside_pair(f, c.inv_eps, hm, hp);
+            hh_out[(size_t)k * plane] = make_float2(hm, hm * ki);
+          }
+        }
         my_count += ((c0 < 0.0f) != (f < 0.0f)) ? 1u : 0u;
         any_bad |= !(fabsf(f) <= 3.402823466e38f);
       }
@@ -382,7 +404,7 @@ __device__ __forceinline__ void zst4_cta(const Geom& g, const Taps& taps, const 
   }
 }
 
-template <int R, int NP>
+template <int R, int NP, bool HH>
 __global__ void __launch_bounds__(Z4<R, NP>::NT, Z4<R, NP>::kMinBlocks)
     zst4_kernel(Geom g, Taps taps, StepConsts c, StepBuffers b, int z_begin, int z_end,
                 const __grid_constant__ CUtensorMap map_phi, const __grid_constant__ CUtensorMap map_ki,
@@ -399,10 +421,10 @@ __global__ void __launch_bounds__(Z4<R, NP>::NT, Z4<R, NP>::kMinBlocks)
   unsigned int my_count = 0;
   const bool interior = x0 >= 2 && x0 + C::TX + 2 <= g.nx && y0 >= 2 && y0 + C::TY + 2 <= g.ny;
   if (interior)
-    zst4_cta<R, NP, false>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
+    zst4_cta<R, NP, false, HH>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
                            &map_p1, smem, my_count);
   else
-    zst4_cta<R, NP, true>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
+    zst4_cta<R, NP, true, HH>(g, taps, c, b, z0, z_stop, x0, y0, bx0, by0, &map_phi, &map_ki, &map_k1i, &map_p0,
                           &map_p1, smem, my_count);
   const unsigned int wsum = __reduce_add_sync(0xffffffffu, my_count);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&s_count, wsum);
@@ -410,12 +432,12 @@ __global__ void __launch_bounds__(Z4<R, NP>::NT, Z4<R, NP>::kMinBlocks)
   if (threadIdx.x == 0 && s_count) atomicAdd(b.counters, (unsigned long long)s_count);
 }
 
-template <int R, int NP>
-int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuffers& b, int z_begin, int z_end,
-                const ZMaps& m, cudaStream_t st) {
+template <int R, int NP, bool HH>
+int zst4_launch_v(const Geom& g, const Taps& t, const StepConsts& c, const StepBuffers& b, int z_begin, int z_end,
+                  const ZMaps& m, cudaStream_t st) {
   using C = Z4<R, NP>;
   if (C::kSmem > 227 * 1024) return -1;
-  auto k = zst4_kernel<R, NP>;
+  auto k = zst4_kernel<R, NP, HH>;
   static bool attr = false;  // benign race: idempotent attribute set
   if (!attr) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem) != cudaSuccess)
@@ -429,10 +451,22 @@ int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuf
   return 1;
 }
 
+// The stored-Heaviside variant exists for the radii where the mode pays
+// (R <= 9, rsfg_api.cu make_xy2_maps); elsewhere b.hh is never set.
+template <int R, int NP>
+int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuffers& b, int z_begin, int z_end,
+                const ZMaps& m, cudaStream_t st) {
+  if constexpr (NP == 1 && R <= 9) {
+    if (b.hh) return zst4_launch_v<R, NP, true>(g, t, c, b, z_begin, z_end, m, st);
+  }
+  if (b.hh) return -1;
+  return zst4_launch_v<R, NP, false>(g, t, c, b, z_begin, z_end, m, st);
+}
+
 }  // namespace
 
 // Per-radius-group entry points (rsfg_zst4_g*.cu): -2 when r is not in the group.
-#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5)
+#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 #define RSFG_ZST4_DECL(N)                                                                              \
   int zst4_group_##N(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c,             \
                      const StepBuffers& b, int z_begin, int z_end, const ZMaps& m, cudaStream_t st);    \

@@ -1,4 +1,4 @@
-// rsfg_zst4_g0.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [0, 1, 2, 3];
+// rsfg_zst4_g0.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [0, 1, 2];
 // split across translation units so the build parallelises.
 #include "rsfg_zst4.cuh"
 
@@ -18,10 +18,6 @@ int zst4_group_box_0(int r, int fields, int* pbox_z, int* ty) {
       *pbox_z = Z4<2, 1>::NW;
       *ty = Z4<2, 1>::TY;
       return (fields == 4 ? Z4<2, 2>::kSmem : Z4<2, 1>::kSmem) <= 227 * 1024;
-    case 3:
-      *pbox_z = Z4<3, 1>::NW;
-      *ty = Z4<3, 1>::TY;
-      return (fields == 4 ? Z4<3, 2>::kSmem : Z4<3, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
   }
@@ -39,9 +35,6 @@ int zst4_group_0(int r, const Geom& g, int fields, const Taps& t1, const StepCon
     case 2:
       return fields == 4 ? zst4_launch<2, 2>(g, t1, c, b, z_begin, z_end, m, st)
                          : zst4_launch<2, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 3:
-      return fields == 4 ? zst4_launch<3, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<3, 1>(g, t1, c, b, z_begin, z_end, m, st);
     default:
       return -2;
   }

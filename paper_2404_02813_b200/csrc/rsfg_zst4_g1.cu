@@ -1,4 +1,4 @@
-// rsfg_zst4_g1.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [4, 5, 6, 7];
+// rsfg_zst4_g1.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [3, 4];
 // split across translation units so the build parallelises.
 #include "rsfg_zst4.cuh"
 
@@ -6,22 +6,14 @@ namespace rsfg {
 
 int zst4_group_box_1(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
+    case 3:
+      *pbox_z = Z4<3, 1>::NW;
+      *ty = Z4<3, 1>::TY;
+      return (fields == 4 ? Z4<3, 2>::kSmem : Z4<3, 1>::kSmem) <= 227 * 1024;
     case 4:
       *pbox_z = Z4<4, 1>::NW;
       *ty = Z4<4, 1>::TY;
       return (fields == 4 ? Z4<4, 2>::kSmem : Z4<4, 1>::kSmem) <= 227 * 1024;
-    case 5:
-      *pbox_z = Z4<5, 1>::NW;
-      *ty = Z4<5, 1>::TY;
-      return (fields == 4 ? Z4<5, 2>::kSmem : Z4<5, 1>::kSmem) <= 227 * 1024;
-    case 6:
-      *pbox_z = Z4<6, 1>::NW;
-      *ty = Z4<6, 1>::TY;
-      return (fields == 4 ? Z4<6, 2>::kSmem : Z4<6, 1>::kSmem) <= 227 * 1024;
-    case 7:
-      *pbox_z = Z4<7, 1>::NW;
-      *ty = Z4<7, 1>::TY;
-      return (fields == 4 ? Z4<7, 2>::kSmem : Z4<7, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
   }
@@ -30,18 +22,12 @@ int zst4_group_box_1(int r, int fields, int* pbox_z, int* ty) {
 int zst4_group_1(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
                   int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
   switch (r) {
+    case 3:
+      return fields == 4 ? zst4_launch<3, 2>(g, t1, c, b, z_begin, z_end, m, st)
+                         : zst4_launch<3, 1>(g, t1, c, b, z_begin, z_end, m, st);
     case 4:
       return fields == 4 ? zst4_launch<4, 2>(g, t1, c, b, z_begin, z_end, m, st)
                          : zst4_launch<4, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 5:
-      return fields == 4 ? zst4_launch<5, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<5, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 6:
-      return fields == 4 ? zst4_launch<6, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<6, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 7:
-      return fields == 4 ? zst4_launch<7, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<7, 1>(g, t1, c, b, z_begin, z_end, m, st);
     default:
       return -2;
   }

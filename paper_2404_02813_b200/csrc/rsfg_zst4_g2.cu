@@ -1,4 +1,4 @@
-// rsfg_zst4_g2.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [8, 9];
+// rsfg_zst4_g2.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [5, 6];
 // split across translation units so the build parallelises.
 #include "rsfg_zst4.cuh"
 
@@ -6,14 +6,14 @@ namespace rsfg {
 
 int zst4_group_box_2(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
-    case 8:
-      *pbox_z = Z4<8, 1>::NW;
-      *ty = Z4<8, 1>::TY;
-      return (fields == 4 ? Z4<8, 2>::kSmem : Z4<8, 1>::kSmem) <= 227 * 1024;
-    case 9:
-      *pbox_z = Z4<9, 1>::NW;
-      *ty = Z4<9, 1>::TY;
-      return (fields == 4 ? Z4<9, 2>::kSmem : Z4<9, 1>::kSmem) <= 227 * 1024;
+    case 5:
+      *pbox_z = Z4<5, 1>::NW;
+      *ty = Z4<5, 1>::TY;
+      return (fields == 4 ? Z4<5, 2>::kSmem : Z4<5, 1>::kSmem) <= 227 * 1024;
+    case 6:
+      *pbox_z = Z4<6, 1>::NW;
+      *ty = Z4<6, 1>::TY;
+      return (fields == 4 ? Z4<6, 2>::kSmem : Z4<6, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
   }
@@ -22,12 +22,12 @@ int zst4_group_box_2(int r, int fields, int* pbox_z, int* ty) {
 int zst4_group_2(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
                   int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
   switch (r) {
-    case 8:
-      return fields == 4 ? zst4_launch<8, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<8, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 9:
-      return fields == 4 ? zst4_launch<9, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<9, 1>(g, t1, c, b, z_begin, z_end, m, st);
+    case 5:
+      return fields == 4 ? zst4_launch<5, 2>(g, t1, c, b, z_begin, z_end, m, st)
+                         : zst4_launch<5, 1>(g, t1, c, b, z_begin, z_end, m, st);
+    case 6:
+      return fields == 4 ? zst4_launch<6, 2>(g, t1, c, b, z_begin, z_end, m, st)
+                         : zst4_launch<6, 1>(g, t1, c, b, z_begin, z_end, m, st);
     default:
       return -2;
   }

@@ -1,4 +1,4 @@
-// rsfg_zst4_g3.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [10, 11];
+// rsfg_zst4_g3.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [7];
 // split across translation units so the build parallelises.
 #include "rsfg_zst4.cuh"
 
@@ -6,14 +6,10 @@ namespace rsfg {
 
 int zst4_group_box_3(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
-    case 10:
-      *pbox_z = Z4<10, 1>::NW;
-      *ty = Z4<10, 1>::TY;
-      return (fields == 4 ? Z4<10, 2>::kSmem : Z4<10, 1>::kSmem) <= 227 * 1024;
-    case 11:
-      *pbox_z = Z4<11, 1>::NW;
-      *ty = Z4<11, 1>::TY;
-      return (fields == 4 ? Z4<11, 2>::kSmem : Z4<11, 1>::kSmem) <= 227 * 1024;
+    case 7:
+      *pbox_z = Z4<7, 1>::NW;
+      *ty = Z4<7, 1>::TY;
+      return (fields == 4 ? Z4<7, 2>::kSmem : Z4<7, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
   }
@@ -22,12 +18,9 @@ int zst4_group_box_3(int r, int fields, int* pbox_z, int* ty) {
 int zst4_group_3(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
                   int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
   switch (r) {
-    case 10:
-      return fields == 4 ? zst4_launch<10, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<10, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 11:
-      return fields == 4 ? zst4_launch<11, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<11, 1>(g, t1, c, b, z_begin, z_end, m, st);
+    case 7:
+      return fields == 4 ? zst4_launch<7, 2>(g, t1, c, b, z_begin, z_end, m, st)
+                         : zst4_launch<7, 1>(g, t1, c, b, z_begin, z_end, m, st);
     default:
       return -2;
   }

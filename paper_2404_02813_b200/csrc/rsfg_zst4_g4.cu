@@ -1,4 +1,4 @@
-// rsfg_zst4_g4.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [12, 15];
+// rsfg_zst4_g4.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [8];
 // split across translation units so the build parallelises.
 #include "rsfg_zst4.cuh"
 
@@ -6,14 +6,10 @@ namespace rsfg {
 
 int zst4_group_box_4(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
-    case 12:
-      *pbox_z = Z4<12, 1>::NW;
-      *ty = Z4<12, 1>::TY;
-      return (fields == 4 ? Z4<12, 2>::kSmem : Z4<12, 1>::kSmem) <= 227 * 1024;
-    case 15:
-      *pbox_z = Z4<15, 1>::NW;
-      *ty = Z4<15, 1>::TY;
-      return (fields == 4 ? Z4<15, 2>::kSmem : Z4<15, 1>::kSmem) <= 227 * 1024;
+    case 8:
+      *pbox_z = Z4<8, 1>::NW;
+      *ty = Z4<8, 1>::TY;
+      return (fields == 4 ? Z4<8, 2>::kSmem : Z4<8, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
   }
@@ -22,12 +18,9 @@ int zst4_group_box_4(int r, int fields, int* pbox_z, int* ty) {
 int zst4_group_4(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
                   int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
   switch (r) {
-    case 12:
-      return fields == 4 ? zst4_launch<12, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<12, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 15:
-      return fields == 4 ? zst4_launch<15, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<15, 1>(g, t1, c, b, z_begin, z_end, m, st);
+    case 8:
+      return fields == 4 ? zst4_launch<8, 2>(g, t1, c, b, z_begin, z_end, m, st)
+                         : zst4_launch<8, 1>(g, t1, c, b, z_begin, z_end, m, st);
     default:
       return -2;
   }

@@ -106,6 +106,29 @@ def test_kernel2_variants_P2(rsf, oracle, zst4, monkeypatch):
     assert _rel_err(st.phi, ref) <= P2_TOL
 
 
+@pytest.mark.parametrize("shape", [(96, 28, 80), (40, 36, 32)])
+def test_stored_heaviside_bitwise(rsf, shape, monkeypatch):
+    """Kernel 2 writing (H-, H- I) for kernel 1 (default for fields=2,
+    sigma2=0) reproduces kernel 1's own Heaviside bit for bit (RSFG_HH=0)."""
+    img, phi, _ = case(*shape)
+    p = _params(rsf, sigma1=3.0, max_iters=6)
+    monkeypatch.setenv("RSFG_HH", "1")
+    a = rsf.evolve(phi, img, p)
+    monkeypatch.setenv("RSFG_HH", "0")
+    b = rsf.evolve(phi, img, p)
+    assert np.array_equal(a, b)
+    # write_phi / blowup rollback invalidate the stored pairs: stepping after an
+    # external phi change must match a fresh state
+    monkeypatch.setenv("RSFG_HH", "1")
+    st = rsf.init_evolution(phi, img, p)
+    st.step()
+    st.phi = np.array(phi)
+    st.step()
+    st2 = rsf.init_evolution(phi, img, p)
+    st2.step()
+    assert np.array_equal(st.phi, st2.phi)
+
+
 @pytest.mark.parametrize("sigma1", [7.0, 2.5])  # R=21 (generic path), R=8
 def test_generic_and_other_radii(rsf, oracle, sigma1):
     from _oracle import params
