@@ -217,6 +217,8 @@ def bench_single(args):
     prof = (C.c_double * 2)()
     check(lib.rsfg_state_profile(h, 10, prof))
     kern = {"xy": prof[0], "zst": prof[1]}
+    vflags, xyb, zstb = C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib.rsfg_state_variant(h, C.byref(vflags), C.byref(xyb), C.byref(zstb)))
     lib.rsfg_state_destroy(h)
     del d_img, d_phi
     torch.cuda.empty_cache()
@@ -224,12 +226,16 @@ def bench_single(args):
     pk, pk_kind = peaks()
     peak = pk["hbm_gbs"]
     dom = max(kern, key=kern.get)
-    kb = KERNEL_BYTES[args.fields]
+    kb = dict(KERNEL_BYTES[args.fields])
+    kb.update(xy=xyb.value, zst=zstb.value)
     achieved = kb[dom] * nvox / (kern[dom] * 1e-3) / 1e9
     traffic = ncu_traffic(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_voxel": kb[dom], "peak_source": f"{pk_kind} hbm_gbs",
+                "kernel_variant_flags": vflags.value,
+                "bytes_note": "per-kernel minimum HBM bytes per voxel (rsfg_state_variant): kernel 2 also "
+                              "writes the (H-, H- I) pairs in the stored-Heaviside mode (flag 4)",
                 "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
                 "kernel_share": {k: round(v / sum(kern.values()), 3) for k, v in kern.items()}}
     step_gbs = ALGO_BYTES_STEP * value / 1e9

@@ -145,6 +145,12 @@ int rsfg_state_stream(rsfg_state* s, void** stream);
 int rsfg_state_sync(rsfg_state* s);
 /* Kernels launched by this state so far. */
 int64_t rsfg_state_launches(const rsfg_state* s);
+/* Kernel variants in use (bit flags): 1 = kernel 1 is the TMA multi-plane
+ * xy2, 2 = kernel 2 is the TMA-fed zst4, 4 = stored-Heaviside mode (kernel 2
+ * writes (H-, H- I) of phi' for kernel 1).  Also each kernel's minimum HBM
+ * bytes per voxel of the owned planes in this configuration. */
+int rsfg_state_variant(const rsfg_state* s, int32_t* flags, int32_t* xy_bytes_per_voxel,
+                       int32_t* zst_bytes_per_voxel);
 void rsfg_state_destroy(rsfg_state* s);
 
 /* ---- z-slab SPMD primitives (multi-GPU) -------------------

@@ -137,6 +137,7 @@ SIGNATURES = {
     "rsfg_state_stream": (C.c_int, [VP, P(VP)]),
     "rsfg_state_sync": (C.c_int, [VP]),
     "rsfg_state_launches": (C.c_int64, [VP]),
+    "rsfg_state_variant": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
     "rsfg_state_destroy": (None, [VP]),
     "rsfg_slab_create": (C.c_int, [P(VP), I32, I32, I32, I32, I32, P(rsfg_params), P(rsfg_options)]),
     "rsfg_slab_geometry": (C.c_int, [VP, P(I32), P(I32), P(I32)]),

@@ -787,6 +787,22 @@ __attribute__((visibility("default"))) int rsfg_state_sync(rsfg_state* st) {
 
 __attribute__((visibility("default"))) int64_t rsfg_state_launches(const rsfg_state* st) { return st ? st->e.launches : 0; }
 
+__attribute__((visibility("default"))) int rsfg_state_variant(const rsfg_state* st, int32_t* flags, int32_t* xyb,
+                                                               int32_t* zstb) {
+  if (!st) return fail(RSFG_ERR_STATE, "null state");
+  const rsfg_slab* s = &st->e;
+  const int f = (s->fast && s->xy2maps[0].valid ? 1 : 0) | (s->fast && s->zmaps[0].valid ? 2 : 0) |
+                (s->hh_mode ? 4 : 0);
+  if (flags) *flags = f;
+  // kernel 1: reads phi + I (or the stored pairs, 8 B either way), writes P
+  // (8 B per field pair); kernel 2: reads P, phi, K2*I (+ K1*I for fields=2),
+  // writes phi' (+ the 8-byte pairs in the stored-Heaviside mode).
+  const int np = s->fields == 4 ? 2 : 1;
+  if (xyb) *xyb = 8 + 8 * np;
+  if (zstb) *zstb = 8 * np + 4 + 4 + (s->fields == 2 ? 4 : 0) + 4 + (s->hh_mode ? 8 : 0);
+  return RSFG_OK;
+}
+
 __attribute__((visibility("default"))) void rsfg_state_destroy(rsfg_state* st) {
   if (!st) return;
   release(&st->e);

@@ -39,7 +39,7 @@ def main():
     out = {"report": a.report, "config": a.config, "kernels": {}}
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
-        key = ("xy" if ("xy_kernel" in name or "xy2_kernel" in name) else
+        key = ("xy" if ("xy_kernel" in name or "xy2_kernel" in name or "xy2_hh_kernel" in name) else
                "zst" if ("zst_kernel" in name or "zst4_kernel" in name) else name[:40])
         d = {}
         for k, (m, _) in KEYS.items():
