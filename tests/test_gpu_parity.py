@@ -239,13 +239,33 @@ def test_cfg1_full_run_P3(rsf, oracle, fields):
 @pytest.mark.parametrize("sigma1", [0.0, 1.0, 3.0, 6.0])
 @pytest.mark.parametrize("fields", [2, 4])
 def test_tma_and_ldg_paths_bitwise(rsf, sigma1, fields, monkeypatch):
-    """Kernel 1 loads its tile by TMA when nx % 4 == 0, else by LDG: same bits."""
+    """The legacy single-plane kernel 1 (RSFG_XY2=0; the path for nx % 4 != 0)
+    loads its tile by TMA (RSFG_TMA=1) or by LDG: same bits."""
     img, phi, _ = case(40, 36, 32)
     p = _params(rsf, sigma1=sigma1, max_iters=3)
+    monkeypatch.setenv("RSFG_XY2", "0")
     a = rsf.evolve(phi, img, p, fields=fields)
     monkeypatch.setenv("RSFG_TMA", "1")
     b = rsf.evolve(phi, img, p, fields=fields)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("fields", [2, 4])
+def test_kernel1_variants_P2(rsf, oracle, fields, monkeypatch):
+    """Kernel 1 as xy2 (default) and as the legacy x-first kernel (RSFG_XY2=0):
+    both within P2 of the oracle after 10 steps."""
+    from _oracle import params
+    img, phi, _ = case(96, 28, 80)
+    op = params(sigma1=3.0)
+    st_o = oracle.init(np.array(img), op)
+    ref = np.array(phi)
+    for _ in range(10):
+        ref, _, _ = oracle.step(ref, np.array(img), op, st_o)
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RSFG_XY2", flag)
+        st = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0), fields=fields)
+        st.run(10)
+        assert _rel_err(st.phi, ref) <= P2_TOL
 
 
 @pytest.mark.parametrize("fields", [2, 4])
