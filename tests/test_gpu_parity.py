@@ -277,3 +277,43 @@ def test_repeat_runs_bitwise(rsf, fields):
     ref = rsf.evolve(phi, img, p, fields=fields)
     for _ in range(3):
         assert np.array_equal(rsf.evolve(phi, img, p, fields=fields), ref)
+
+
+def test_evolve_convergence_stop(rsf):
+    """convergence_fraction (rsf.cpp:378): evolve stops after the first step whose
+    sign-change fraction falls below it -- the same step stepping finds."""
+    img, phi, _ = case(40, 36, 32)
+    fracs = []
+    st = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0))
+    for _ in range(40):
+        fracs.append(st.step())
+    cf = sorted(fracs)[len(fracs) // 2]  # reached part-way through
+    first = next(i for i, f in enumerate(fracs) if f < cf) + 1
+    from paper_2404_02813_b200 import _lib as L
+    rep = L.rsfg_report()
+    got = rsf.evolve(phi, img, _params(rsf, sigma1=3.0, max_iters=40, convergence_fraction=cf), report=rep)
+    assert rep.iterations == first
+    st2 = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0))
+    for _ in range(first):
+        st2.step()
+    assert np.array_equal(got, st2.phi)
+
+
+def test_evolve_stop_callback(rsf):
+    """StopCheck every stop_every iterations with the current phi (rsf.cpp:379-381)."""
+    img, phi, _ = case(40, 36, 32)
+    seen = []
+
+    def stop(cur, it):
+        seen.append((it, cur.copy()))
+        return it >= 10
+
+    got = rsf.evolve(phi, img, _params(rsf, sigma1=3.0, max_iters=30), stop=stop, stop_every=5)
+    assert [it for it, _ in seen] == [5, 10]
+    st = rsf.init_evolution(phi, img, _params(rsf, sigma1=3.0))
+    for i in range(10):
+        st.step()
+        if i == 4:
+            assert np.array_equal(seen[0][1], st.phi)
+    assert np.array_equal(seen[1][1], st.phi)
+    assert np.array_equal(got, st.phi)
