@@ -49,11 +49,19 @@ __global__ void conv_axis_kernel(Geom g, Taps taps, int axis, const T* __restric
     const int n_ax = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
     T acc;
     const int lo = axis == 2 ? g.zb : 0, hi = axis == 2 ? g.ze - 1 : n_ax - 1;
-    for (int j = 0; j <= 2 * r; ++j) {
-      const int q = clampi(clampi(pos - r + j, 0, n_ax - 1), lo, hi);
-      const size_t s = axis == 0 ? vidx(g, q, y, z) : (axis == 1 ? vidx(g, x, q, z) : vidx(g, x, y, q));
-      const T v = src[s];
-      acc = j == 0 ? tap<T>(taps.w[0], v) : fma_t(taps.w[j], v, acc);
+    if (pos - r >= max(lo, 0) && pos + r <= min(hi, n_ax - 1)) {
+      // whole window inside: one base pointer, constant stride, no clamps
+      const long long stride = axis == 0 ? 1 : (axis == 1 ? g.nx : g.plane);
+      const T* p = src + (long long)vidx(g, x, y, z) - (long long)r * stride;
+      acc = tap<T>(taps.w[0], p[0]);
+      for (int j = 1; j <= 2 * r; ++j) acc = fma_t(taps.w[j], p[j * stride], acc);
+    } else {
+      for (int j = 0; j <= 2 * r; ++j) {
+        const int q = clampi(clampi(pos - r + j, 0, n_ax - 1), lo, hi);
+        const size_t sidx = axis == 0 ? vidx(g, q, y, z) : (axis == 1 ? vidx(g, x, q, z) : vidx(g, x, y, q));
+        const T v = src[sidx];
+        acc = j == 0 ? tap<T>(taps.w[0], v) : fma_t(taps.w[j], v, acc);
+      }
     }
     dst[vidx(g, x, y, z)] = acc;
   }
