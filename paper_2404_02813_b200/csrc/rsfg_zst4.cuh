@@ -32,12 +32,19 @@
 namespace rsfg {
 namespace {
 
+#ifndef RSFG_Z4_TALL_TY
+#define RSFG_Z4_TALL_TY 8
+#endif
+// column-tile height for R <= 9, fields=2: 32 x 16 (one 512-thread CTA/SM,
+// halo = 3 full warps) measured slower than 32 x 8 (zst 1.044 vs 0.962 ms)
+constexpr int kZ4TallTY = RSFG_Z4_TALL_TY;
+
 template <int R, int NP>
 struct Z4 {
   // 32 x 8 columns; 32 x 4 for large radii, whose z-pass window (8 + 2R
   // planes of P) would otherwise leave one CTA per SM.
-  static constexpr int TX = 32, TY = R >= 17 ? 4 : 8, NT = TX * TY;
-  static constexpr int kMinBlocks = TY == 4 && NP == 1 ? 3 : 2;  // CTAs per SM the registers must allow
+  static constexpr int TX = 32, TY = R >= 17 ? 4 : (R <= 9 && NP == 1 ? kZ4TallTY : 8), NT = TX * TY;
+  static constexpr int kMinBlocks = TY == 16 ? 1 : (TY == 4 && NP == 1 ? 3 : 2);  // CTAs per SM for the registers
   static constexpr int BX = 40, BY = TY + 4, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)

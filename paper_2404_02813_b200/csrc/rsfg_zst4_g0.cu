@@ -8,15 +8,15 @@ int zst4_group_box_0(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 0:
       *pbox_z = Z4<0, 1>::NW;
-      *ty = Z4<0, 1>::TY;
+      *ty = fields == 4 ? Z4<0, 2>::TY : Z4<0, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<0, 2>::kSmem : Z4<0, 1>::kSmem) <= 227 * 1024;
     case 1:
       *pbox_z = Z4<1, 1>::NW;
-      *ty = Z4<1, 1>::TY;
+      *ty = fields == 4 ? Z4<1, 2>::TY : Z4<1, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<1, 2>::kSmem : Z4<1, 1>::kSmem) <= 227 * 1024;
     case 2:
       *pbox_z = Z4<2, 1>::NW;
-      *ty = Z4<2, 1>::TY;
+      *ty = fields == 4 ? Z4<2, 2>::TY : Z4<2, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<2, 2>::kSmem : Z4<2, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -8,11 +8,11 @@ int zst4_group_box_1(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 3:
       *pbox_z = Z4<3, 1>::NW;
-      *ty = Z4<3, 1>::TY;
+      *ty = fields == 4 ? Z4<3, 2>::TY : Z4<3, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<3, 2>::kSmem : Z4<3, 1>::kSmem) <= 227 * 1024;
     case 4:
       *pbox_z = Z4<4, 1>::NW;
-      *ty = Z4<4, 1>::TY;
+      *ty = fields == 4 ? Z4<4, 2>::TY : Z4<4, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<4, 2>::kSmem : Z4<4, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -8,11 +8,11 @@ int zst4_group_box_2(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 5:
       *pbox_z = Z4<5, 1>::NW;
-      *ty = Z4<5, 1>::TY;
+      *ty = fields == 4 ? Z4<5, 2>::TY : Z4<5, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<5, 2>::kSmem : Z4<5, 1>::kSmem) <= 227 * 1024;
     case 6:
       *pbox_z = Z4<6, 1>::NW;
-      *ty = Z4<6, 1>::TY;
+      *ty = fields == 4 ? Z4<6, 2>::TY : Z4<6, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<6, 2>::kSmem : Z4<6, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

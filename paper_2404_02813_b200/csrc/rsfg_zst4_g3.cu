@@ -8,7 +8,7 @@ int zst4_group_box_3(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 7:
       *pbox_z = Z4<7, 1>::NW;
-      *ty = Z4<7, 1>::TY;
+      *ty = fields == 4 ? Z4<7, 2>::TY : Z4<7, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<7, 2>::kSmem : Z4<7, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -8,11 +8,11 @@ int zst4_group_box_6(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 10:
       *pbox_z = Z4<10, 1>::NW;
-      *ty = Z4<10, 1>::TY;
+      *ty = fields == 4 ? Z4<10, 2>::TY : Z4<10, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<10, 2>::kSmem : Z4<10, 1>::kSmem) <= 227 * 1024;
     case 11:
       *pbox_z = Z4<11, 1>::NW;
-      *ty = Z4<11, 1>::TY;
+      *ty = fields == 4 ? Z4<11, 2>::TY : Z4<11, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<11, 2>::kSmem : Z4<11, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -8,11 +8,11 @@ int zst4_group_box_7(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 12:
       *pbox_z = Z4<12, 1>::NW;
-      *ty = Z4<12, 1>::TY;
+      *ty = fields == 4 ? Z4<12, 2>::TY : Z4<12, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<12, 2>::kSmem : Z4<12, 1>::kSmem) <= 227 * 1024;
     case 15:
       *pbox_z = Z4<15, 1>::NW;
-      *ty = Z4<15, 1>::TY;
+      *ty = fields == 4 ? Z4<15, 2>::TY : Z4<15, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<15, 2>::kSmem : Z4<15, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;

@@ -8,7 +8,7 @@ int zst4_group_box_8(int r, int fields, int* pbox_z, int* ty) {
   switch (r) {
     case 18:
       *pbox_z = Z4<18, 1>::NW;
-      *ty = Z4<18, 1>::TY;
+      *ty = fields == 4 ? Z4<18, 2>::TY : Z4<18, 1>::TY;  // box rows = the launched kernel's tile
       return (fields == 4 ? Z4<18, 2>::kSmem : Z4<18, 1>::kSmem) <= 227 * 1024;
     default:
       return -2;
