@@ -15,6 +15,20 @@ namespace {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+// Opt a kernel into `bytes` of dynamic shared memory, once per (kernel,
+// device): the attribute is per device, so a process that drives several GPUs
+// sets it on each (a benign race otherwise: the set is idempotent).
+template <auto Kernel>
+inline bool smem_optin(int bytes) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && done[dev]) return true;
+  if (cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return true;
+}
+
 __device__ __forceinline__ size_t vidx(const Geom& g, int x, int y, int z) {
   return (size_t)(z - g.zb) * (size_t)g.plane + (size_t)y * (size_t)g.nx + (size_t)x;
 }

@@ -160,11 +160,7 @@ int xy_launch(const Geom& g, const Taps& t, float inv_eps, const float* phi, con
               float2* P1, int z_begin, int z_end, const XYMaps* maps, cudaStream_t st) {
   using C = XYCfg<R, NP, kXYTX, kXYTY, kBX, kBY>;
   auto k = xy_kernel<R, NP, kXYTX, kXYTY, kBX, kBY, TMA>;
-  static bool attr = false;  // benign race: idempotent attribute set
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-    attr = true;
-  }
+  smem_optin<xy_kernel<R, NP, kXYTX, kXYTY, kBX, kBY, TMA>>((int)C::kSmem);
   if (z_end <= z_begin) return 0;
   static const CUtensorMap kNoMap{};
   const CUtensorMap& mp = TMA ? maps->phi : kNoMap;

@@ -458,12 +458,7 @@ int xy2_hh_launch(const Geom& g, const Taps& t, float2* P0, int z_begin, int z_e
   using C = XY2<R, 1, TY>;
   if (C::kSmemHH > 227 * 1024) return -1;
   auto k = xy2_hh_kernel<R, TY>;
-  static bool attr = false;  // benign race: idempotent attribute set
-  if (!attr) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmemHH) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  if (!smem_optin<xy2_hh_kernel<R, TY>>((int)C::kSmemHH)) return -1;
   if (z_end <= z_begin) return 0;
   dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
   k<<<grid, C::NT, C::kSmemHH, st>>>(g, t, P0, z_begin, z_end, m.hh);
@@ -482,12 +477,7 @@ int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* 
   using C = XY2<R, NP, TY>;
   if (C::kSmem > 227 * 1024) return -1;
   auto k = xy2_kernel<R, NP, TY>;
-  static bool attr = false;  // benign race: idempotent attribute set
-  if (!attr) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  if (!smem_optin<xy2_kernel<R, NP, TY>>((int)C::kSmem)) return -1;
   if (z_end <= z_begin) return 0;
   dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
   k<<<grid, C::NT, C::kSmem, st>>>(g, t, inv_eps, P0, P1, z_begin, z_end, m.phi, m.img);

@@ -303,11 +303,7 @@ int zst_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuff
   constexpr int NCH = kZTZC * kZNCH / TZC;
   using C = ZCfg<R, NP, kZTX, kZTY, TZC, NCH>;
   auto k = zst_kernel<R, NP, kZTX, kZTY, TZC, NCH>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-    attr = true;
-  }
+  smem_optin<zst_kernel<R, NP, kZTX, kZTY, TZC, NCH>>((int)C::kSmem);
   if (z_end <= z_begin) return 0;
   dim3 grid((z_end - z_begin + C::TZ - 1) / C::TZ, (g.nx + kZTX - 1) / kZTX, (g.ny + kZTY - 1) / kZTY);
   k<<<grid, kZTX * kZTY, C::kSmem, st>>>(g, t, c, b, z_begin, z_end, mode);

@@ -445,12 +445,7 @@ int zst4_launch_v(const Geom& g, const Taps& t, const StepConsts& c, const StepB
   using C = Z4<R, NP>;
   if (C::kSmem > 227 * 1024) return -1;
   auto k = zst4_kernel<R, NP, HH>;
-  static bool attr = false;  // benign race: idempotent attribute set
-  if (!attr) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  if (!smem_optin<zst4_kernel<R, NP, HH>>((int)C::kSmem)) return -1;
   if (z_end <= z_begin) return 0;
   dim3 grid((z_end - z_begin + C::TZ - 1) / C::TZ, (g.nx + C::TX - 1) / C::TX, (g.ny + C::TY - 1) / C::TY);
   k<<<grid, C::NT, C::kSmem, st>>>(g, t, c, b, z_begin, z_end, m.phi, m.ki, NP == 1 ? m.k1i : m.ki, m.p[0],
