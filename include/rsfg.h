@@ -237,6 +237,10 @@ void rsfg_blob_params_default(rsfg_blob_params* b);
 int rsfg_init_phi_device(const float* d_image, int32_t nx, int32_t ny, int32_t nz, const rsfg_blob_params* bp,
                          double seed_radius, float* d_phi0, int32_t device, int32_t* n_seeds, int32_t* seeds_xyz,
                          float* seeds_resp, int32_t cap, int32_t* iterations);
+/* Same with HOST buffers (image in, phi0 out); device buffers are internal. */
+int rsfg_init_phi(const float* image, int32_t nx, int32_t ny, int32_t nz, const rsfg_blob_params* bp,
+                  double seed_radius, float* phi0, int32_t device, int32_t* n_seeds, int32_t* seeds_xyz,
+                  float* seeds_resp, int32_t cap, int32_t* iterations);
 
 /* ---- curtain tiling around the hot path (tiling.hpp:12-71) -- */
 typedef struct rsfg_tile { /* rsf::TileBox (tiling.hpp:13-17); axes x, y, z */

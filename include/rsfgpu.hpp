@@ -1,11 +1,13 @@
 // rsfgpu.hpp -- header-only C++ wrapper over the C-ABI (rsfg.h) with the
 // reference's exact C++ surface: the same function names, argument meaning,
 // defaults and exception types as /root/reference/proj/include/rsf/rsf.hpp
-// (RsfParams, evolve, init_evolution, evolve_step, energy, extract_mask) in
-// namespace rsfgpu.  A caller of rsf::evolve switches by changing the
+// (RsfParams, evolve, init_evolution, evolve_step, energy, extract_mask) and
+// of seeding.hpp / tiling.hpp (BlobParams, init_phi, plan_tiles,
+// run_pipeline) in namespace rsfgpu.  A caller of rsf::evolve switches by changing the
 // namespace (and linking librsfg.so); see INTEGRATION.md.
 #pragma once
 
+#include <algorithm>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -35,6 +37,10 @@ class cuda_error : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
+class io_error : public std::runtime_error {  // rsf::io_error (core.hpp:23-26)
+ public:
+  using std::runtime_error::runtime_error;
+};
 
 inline void check(int rc) {
   if (rc == RSFG_OK) return;
@@ -43,6 +49,7 @@ inline void check(int rc) {
     case RSFG_ERR_PARAM: throw param_error(msg);
     case RSFG_ERR_SHAPE: throw shape_error(msg);
     case RSFG_ERR_BLOWUP: throw blowup_error(msg);
+    case RSFG_ERR_IO: throw io_error(msg);
     default: throw cuda_error(msg);
   }
 }
@@ -175,6 +182,140 @@ inline Volume energy(EvolutionState& st) {
   Volume E(st.dims_.nx, st.dims_.ny, st.dims_.nz);
   check(rsfg_state_energy(st.s_, E.data.data()));
   return E;
+}
+
+// ---- seeding and curtain tiling around the hot path ------
+
+enum class Polarity { bright_on_dark, dark_on_bright };  // seeding.hpp:10
+
+// rsf::BlobParams (seeding.hpp:12-20), same defaults.
+struct BlobParams {
+  double sigma_b = 3.0;
+  double response_threshold = 0.1;
+  double nms_radius = 0.0;
+  Polarity polarity = Polarity::bright_on_dark;
+  double resolved_nms_radius() const { return nms_radius > 0.0 ? nms_radius : 2.0 * sigma_b; }
+  rsfg_blob_params c() const {
+    return rsfg_blob_params{sigma_b, response_threshold, nms_radius, polarity == Polarity::dark_on_bright ? 1 : 0};
+  }
+};
+
+struct Seed {  // seeding.hpp:22-25
+  int x = 0, y = 0, z = 0;
+  float response = 0.0f;
+};
+struct SeedSet {  // seeding.hpp:27-31
+  std::vector<Seed> points;
+  double detection_scale = 0.0;
+  double response_threshold = 0.0;
+};
+
+// rsf::init_phi (seeding.hpp:60-61, seeding.cpp:221-235): seeds and the
+// distance field computed on the GPU; same seeds, same order.
+inline std::pair<Volume, SeedSet> init_phi(const Volume& vol, const BlobParams& bp, double seed_radius = 2.0,
+                                           int device = 0) {
+  const rsfg_blob_params cb = bp.c();
+  Volume phi(vol.dims.nx, vol.dims.ny, vol.dims.nz);
+  int32_t cap = (int32_t)std::min<std::size_t>(vol.voxels(), 1u << 16), n = 0, it = 0;
+  std::vector<int32_t> xyz;
+  std::vector<float> resp;
+  for (;;) {
+    xyz.assign(3 * (std::size_t)cap, 0);
+    resp.assign(cap, 0.0f);
+    check(rsfg_init_phi(vol.data.data(), vol.dims.nx, vol.dims.ny, vol.dims.nz, &cb, seed_radius, phi.data.data(),
+                        device, &n, xyz.data(), resp.data(), cap, &it));
+    if (n <= cap) break;
+    cap = n;  // more seeds than the first buffer held: rerun with room for all
+  }
+  SeedSet s;
+  s.detection_scale = bp.sigma_b;
+  s.response_threshold = bp.response_threshold;
+  s.points.resize(n);
+  for (int32_t k = 0; k < n; ++k) s.points[k] = Seed{xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2], resp[k]};
+  return {std::move(phi), std::move(s)};
+}
+
+struct TileBox {  // tiling.hpp:13-17
+  int ix = 0, iy = 0, iz = 0;
+  Dims core_origin, core_extent;
+  Dims pad_origin, pad_extent;
+};
+struct TileLayout {  // tiling.hpp:19-24
+  Dims vol_dims;
+  Dims tile_size;
+  int curtain = 0;
+  std::vector<TileBox> tiles;
+};
+enum class MergeMode { linear, minimum, maximum, average };  // tiling.hpp:26
+
+// rsf::plan_tiles (tiling.hpp:28-30, tiling.cpp:14-59).
+inline TileLayout plan_tiles(Dims dims, Dims tile_size, double sigma1, double sigma2) {
+  TileLayout L;
+  L.vol_dims = dims;
+  L.tile_size = tile_size;
+  int32_t n = 0, curtain = 0;
+  check(rsfg_plan_tiles(dims.nx, dims.ny, dims.nz, tile_size.nx, tile_size.ny, tile_size.nz, sigma1, sigma2, nullptr,
+                        0, &n, &curtain));
+  std::vector<rsfg_tile> t(n);
+  check(rsfg_plan_tiles(dims.nx, dims.ny, dims.nz, tile_size.nx, tile_size.ny, tile_size.nz, sigma1, sigma2, t.data(),
+                        n, &n, &curtain));
+  L.curtain = curtain;
+  for (const rsfg_tile& c : t)
+    L.tiles.push_back(TileBox{c.ix, c.iy, c.iz, Dims{c.core_origin[0], c.core_origin[1], c.core_origin[2]},
+                              Dims{c.core_extent[0], c.core_extent[1], c.core_extent[2]},
+                              Dims{c.pad_origin[0], c.pad_origin[1], c.pad_origin[2]},
+                              Dims{c.pad_extent[0], c.pad_extent[1], c.pad_extent[2]}});
+  return L;
+}
+
+struct PipelineOptions {  // tiling.hpp:41-47 (spill_dir has no device counterpart)
+  bool global_seeding = false;
+  MergeMode merge = MergeMode::linear;
+  BlobParams blob;
+  double seed_radius = 2.0;
+  int device = 0;
+  int fields = RSFG_FIELDS_2;
+};
+struct PipelineResult {  // tiling.hpp:49-53
+  Volume phi;
+  Volume mask;
+  std::vector<std::string> warnings;
+};
+
+// rsf::run_pipeline (tiling.hpp:58-60, tiling.cpp:201-275): every tile is
+// seeded, initialised and evolved on one GPU, then merged on the device.
+// `workers` is accepted for signature parity; tiles run back to back on the
+// device (the output never depended on the worker count).
+inline PipelineResult run_pipeline(const Volume& vol, const RsfParams& rsf_params, const BlobParams& blob_params,
+                                   const TileLayout& layout, int workers, const PipelineOptions& opts = {}) {
+  (void)workers;
+  rsf_params.validate();
+  if (!(layout.vol_dims == vol.dims)) throw shape_error("run_pipeline: layout does not match the volume");
+  const rsfg_params cp = rsf_params.c();
+  const rsfg_blob_params cb = blob_params.c();
+  rsfg_pipeline_options o;
+  rsfg_pipeline_options_default(&o);
+  o.global_seeding = opts.global_seeding ? 1 : 0;
+  o.merge = (int32_t)opts.merge;
+  o.seed_radius = opts.seed_radius;
+  o.device = opts.device;
+  o.fields = opts.fields;
+  PipelineResult r;
+  r.phi = Volume(vol.dims.nx, vol.dims.ny, vol.dims.nz);
+  r.mask = Volume(vol.dims.nx, vol.dims.ny, vol.dims.nz);
+  std::vector<char> w(1 << 16, 0);
+  int32_t nw = 0;
+  check(rsfg_run_pipeline(vol.data.data(), vol.dims.nx, vol.dims.ny, vol.dims.nz, &cp, &cb, layout.tile_size.nx,
+                          layout.tile_size.ny, layout.tile_size.nz, &o, r.phi.data.data(), r.mask.data.data(),
+                          w.data(), (int32_t)w.size(), &nw));
+  std::string all(w.data());
+  for (std::size_t a = 0; a < all.size();) {
+    std::size_t b = all.find('\n', a);
+    if (b == std::string::npos) b = all.size();
+    if (b > a) r.warnings.push_back(all.substr(a, b - a));
+    a = b + 1;
+  }
+  return r;
 }
 
 }  // namespace rsfgpu

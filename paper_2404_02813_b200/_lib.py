@@ -171,6 +171,8 @@ SIGNATURES = {
                                     P(rsfg_pipeline_options), FP, FP, C.c_char_p, I32, P(I32)]),
     "rsfg_init_phi_device": (C.c_int, [VP, I32, I32, I32, P(rsfg_blob_params), C.c_double, VP, I32, P(I32),
                                        P(I32), FP, I32, P(I32)]),
+    "rsfg_init_phi": (C.c_int, [FP, I32, I32, I32, P(rsfg_blob_params), C.c_double, FP, I32, P(I32),
+                                P(I32), FP, I32, P(I32)]),
 }
 
 _lib = None

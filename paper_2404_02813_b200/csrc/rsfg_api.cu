@@ -1195,4 +1195,35 @@ __attribute__((visibility("default"))) int rsfg_init_phi_device(const float* d_i
   return RSFG_OK;
 }
 
+// rsf::init_phi with HOST buffers (seeding.cpp:221-235): the image goes up,
+// seeding and the distance run on the device, phi0 comes back.
+__attribute__((visibility("default"))) int rsfg_init_phi(const float* image, int32_t nx, int32_t ny, int32_t nz,
+                                                         const rsfg_blob_params* bp, double seed_radius,
+                                                         float* phi0, int32_t device, int32_t* n_seeds,
+                                                         int32_t* seeds_xyz, float* seeds_resp, int32_t cap,
+                                                         int32_t* iterations) {
+  if (!image || !phi0) return fail(RSFG_ERR_STATE, "init_phi: null buffer");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return fail(RSFG_ERR_SHAPE, "volume dims must be positive");
+  CUDA_TRY(cudaSetDevice(device));
+  const size_t bytes = (size_t)nx * ny * nz * sizeof(float);
+  float* d_img = nullptr;
+  float* d_phi = nullptr;
+  if (cudaMalloc(&d_img, bytes) != cudaSuccess || cudaMalloc(&d_phi, bytes) != cudaSuccess) {
+    cudaFree(d_img);
+    cudaFree(d_phi);
+    return fail(RSFG_ERR_OOM, "init_phi: out of device memory");
+  }
+  int rc = RSFG_OK;
+  if (cudaMemcpy(d_img, image, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(RSFG_ERR_CUDA, "init_phi: upload failed");
+  if (!rc)
+    rc = rsfg_init_phi_device(d_img, nx, ny, nz, bp, seed_radius, d_phi, device, n_seeds, seeds_xyz, seeds_resp,
+                              cap, iterations);
+  if (!rc && cudaMemcpy(phi0, d_phi, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(RSFG_ERR_CUDA, "init_phi: download failed");
+  cudaFree(d_img);
+  cudaFree(d_phi);
+  return rc;
+}
+
 }  // extern "C"
