@@ -871,12 +871,34 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
       }
     }
   } sguard{st, opt.reuse_workspace != 0};
+  // The image goes up first; phi0's upload then runs on a side stream under
+  // the image range + static convolutions (which do not read phi), and the
+  // loop waits for it.  ms_h2d is the image upload, ms_init the overlapped
+  // init + phi0 upload.
+  cudaStream_t side = nullptr;
+  cudaEvent_t phi_up = nullptr;
+  struct SideGuard {
+    cudaStream_t* st;
+    cudaEvent_t* e;
+    ~SideGuard() {
+      if (*st) cudaStreamDestroy(*st);
+      if (*e) cudaEventDestroy(*e);
+    }
+  } side_guard{&side, &phi_up};
+  CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&phi_up, cudaEventDisableTiming));
+  const size_t held_bytes = s->held() * sizeof(float);
+  s->hh_valid = false;
   cudaEventRecord(ev[0], s->stream);
-  if (int rc = upload(s, phi, image, cudaMemcpyHostToDevice)) return rc;
+  CUDA_TRY(cudaMemcpyAsync(s->image, image, held_bytes, cudaMemcpyHostToDevice, s->stream));
   cudaEventRecord(ev[1], s->stream);
   float lo, hi;
   if (int rc = local_range(s, &lo, &hi)) return rc;
   if (int rc = init_static(s, lo, hi)) return rc;
+  CUDA_TRY(cudaStreamWaitEvent(side, ev[0], 0));  // after setup's memsets of phi[]
+  CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, held_bytes, cudaMemcpyHostToDevice, side));
+  CUDA_TRY(cudaEventRecord(phi_up, side));
+  CUDA_TRY(cudaStreamWaitEvent(s->stream, phi_up, 0));
   cudaEventRecord(ev[2], s->stream);
 
   const bool per_step = p->convergence_fraction > 0.0;
