@@ -258,6 +258,9 @@ typedef struct rsfg_pipeline_options { /* rsf::PipelineOptions (tiling.hpp:41-47
   double seed_radius;  /* default 2                                      */
   int32_t device;
   int32_t fields;      /* RSFG_FIELDS_2 (default) or RSFG_FIELDS_4       */
+  const char* spill_dir; /* when non-NULL/non-empty: every tile's phi is written
+                            there as tile_zZZ_yYY_xXX.vmh, then layout.manifest
+                            (tiling.cpp:256-263)                            */
 } rsfg_pipeline_options;
 void rsfg_pipeline_options_default(rsfg_pipeline_options* o);
 /* plan_tiles (tiling.cpp:14-59): core tiles of tile size (tx, ty, tz) with a
@@ -278,6 +281,27 @@ int rsfg_run_pipeline(const float* image, int32_t nx, int32_t ny, int32_t nz, co
                       const rsfg_blob_params* bp, int32_t tx, int32_t ty, int32_t tz,
                       const rsfg_pipeline_options* o, float* phi, float* mask, char* warnings,
                       int32_t warnings_cap, int32_t* n_warnings);
+
+/* tile_file_name (tiling.cpp:195-199): "tile_zZZ_yYY_xXX.vmh" into buf. */
+int rsfg_tile_file_name(const rsfg_tile* t, char* buf, int32_t cap);
+/* save_manifest / load_manifest (tiling.cpp:277-321): the reference's text
+ * format; load fills dims3, tile_size3, curtain and up to cap tiles (*n_tiles
+ * = the full count).  Failures are RSFG_ERR_IO with the reference's messages. */
+int rsfg_save_manifest(const char* path, int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t ty, int32_t tz,
+                       int32_t curtain, const rsfg_tile* tiles, int32_t n_tiles);
+int rsfg_load_manifest(const char* path, int32_t* dims3, int32_t* tile_size3, int32_t* curtain, rsfg_tile* tiles,
+                       int32_t cap, int32_t* n_tiles);
+/* merge_from_dir (tiling.cpp:323-332): reads every tile of the layout (dims,
+ * tile size, curtain, tiles -- rsfg_plan_tiles or rsfg_load_manifest) from
+ * dir/tile_file_name straight into device buffers and merges them on the
+ * device into d_out (nx*ny*nz floats). */
+int rsfg_merge_from_dir(const char* dir, int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t ty, int32_t tz,
+                        int32_t curtain, const rsfg_tile* tiles, int32_t n_tiles, int32_t mode, float* d_out,
+                        int32_t device);
+/* Same into a HOST buffer (rsf::merge_from_dir returns a host Volume). */
+int rsfg_merge_from_dir_host(const char* dir, int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t ty,
+                             int32_t tz, int32_t curtain, const rsfg_tile* tiles, int32_t n_tiles, int32_t mode,
+                             float* out, int32_t device);
 
 /* ---- volume I/O and overlap metrics ------------------ */
 /* read_volume's header (volume_io.cpp:24-76): dims, spacing, payload width. */

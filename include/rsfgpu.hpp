@@ -268,11 +268,66 @@ inline TileLayout plan_tiles(Dims dims, Dims tile_size, double sigma1, double si
   return L;
 }
 
-struct PipelineOptions {  // tiling.hpp:41-47 (spill_dir has no device counterpart)
+inline rsfg_tile c_tile(const TileBox& t) {
+  return rsfg_tile{t.ix, t.iy, t.iz, {t.core_origin.nx, t.core_origin.ny, t.core_origin.nz},
+                   {t.core_extent.nx, t.core_extent.ny, t.core_extent.nz},
+                   {t.pad_origin.nx, t.pad_origin.ny, t.pad_origin.nz},
+                   {t.pad_extent.nx, t.pad_extent.ny, t.pad_extent.nz}};
+}
+inline std::vector<rsfg_tile> c_tiles(const TileLayout& L) {
+  std::vector<rsfg_tile> v;
+  for (const TileBox& t : L.tiles) v.push_back(c_tile(t));
+  return v;
+}
+
+// rsf::tile_file_name (tiling.cpp:195-199).
+inline std::string tile_file_name(const TileBox& t) {
+  char buf[64];
+  const rsfg_tile c = c_tile(t);
+  check(rsfg_tile_file_name(&c, buf, sizeof buf));
+  return buf;
+}
+
+// rsf::save_manifest / load_manifest (tiling.cpp:277-321); paths as strings.
+inline void save_manifest(const std::string& path, const TileLayout& L) {
+  const std::vector<rsfg_tile> v = c_tiles(L);
+  check(rsfg_save_manifest(path.c_str(), L.vol_dims.nx, L.vol_dims.ny, L.vol_dims.nz, L.tile_size.nx,
+                           L.tile_size.ny, L.tile_size.nz, L.curtain, v.data(), (int32_t)v.size()));
+}
+inline TileLayout load_manifest(const std::string& path) {
+  int32_t d[3], ts[3], c = 0, n = 0;
+  check(rsfg_load_manifest(path.c_str(), d, ts, &c, nullptr, 0, &n));
+  std::vector<rsfg_tile> v(n);
+  check(rsfg_load_manifest(path.c_str(), d, ts, &c, v.data(), n, &n));
+  TileLayout L;
+  L.vol_dims = Dims{d[0], d[1], d[2]};
+  L.tile_size = Dims{ts[0], ts[1], ts[2]};
+  L.curtain = c;
+  for (const rsfg_tile& t : v)
+    L.tiles.push_back(TileBox{t.ix, t.iy, t.iz, Dims{t.core_origin[0], t.core_origin[1], t.core_origin[2]},
+                              Dims{t.core_extent[0], t.core_extent[1], t.core_extent[2]},
+                              Dims{t.pad_origin[0], t.pad_origin[1], t.pad_origin[2]},
+                              Dims{t.pad_extent[0], t.pad_extent[1], t.pad_extent[2]}});
+  return L;
+}
+
+// rsf::merge_from_dir (tiling.cpp:323-332): tiles read and merged on the GPU.
+inline Volume merge_from_dir(const std::string& dir, const TileLayout& L, MergeMode mode = MergeMode::linear,
+                             int device = 0) {
+  const std::vector<rsfg_tile> v = c_tiles(L);
+  Volume out(L.vol_dims.nx, L.vol_dims.ny, L.vol_dims.nz);
+  check(rsfg_merge_from_dir_host(dir.c_str(), L.vol_dims.nx, L.vol_dims.ny, L.vol_dims.nz, L.tile_size.nx,
+                                 L.tile_size.ny, L.tile_size.nz, L.curtain, v.data(), (int32_t)v.size(),
+                                 (int32_t)mode, out.data.data(), device));
+  return out;
+}
+
+struct PipelineOptions {  // tiling.hpp:41-47
   bool global_seeding = false;
   MergeMode merge = MergeMode::linear;
   BlobParams blob;
   double seed_radius = 2.0;
+  std::string spill_dir;  // when set, per-tile phi is written here + manifest
   int device = 0;
   int fields = RSFG_FIELDS_2;
 };
@@ -300,6 +355,7 @@ inline PipelineResult run_pipeline(const Volume& vol, const RsfParams& rsf_param
   o.seed_radius = opts.seed_radius;
   o.device = opts.device;
   o.fields = opts.fields;
+  o.spill_dir = opts.spill_dir.empty() ? nullptr : opts.spill_dir.c_str();
   PipelineResult r;
   r.phi = Volume(vol.dims.nx, vol.dims.ny, vol.dims.nz);
   r.mask = Volume(vol.dims.nx, vol.dims.ny, vol.dims.nz);

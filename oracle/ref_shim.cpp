@@ -270,6 +270,22 @@ int rsfref_run_pipeline(const float* image, int nx, int ny, int nz, const RefPar
   })
 }
 
+// save_manifest (tiling.cpp:277-295) of plan_tiles(dims, tile, sigma1, sigma2).
+int rsfref_save_manifest(const char* path, int nx, int ny, int nz, int tx, int ty, int tz, double sigma1,
+                         double sigma2) {
+  GUARD({ rsf::save_manifest(path, rsf::plan_tiles({nx, ny, nz}, {tx, ty, tz}, sigma1, sigma2)); })
+}
+
+// load_manifest + merge_from_dir (tiling.cpp:297-332) into out.
+int rsfref_merge_from_dir(const char* dir, const char* manifest, int mode, float* out, long cap) {
+  GUARD({
+    const rsf::TileLayout L = rsf::load_manifest(manifest);
+    rsf::Volume m = rsf::merge_from_dir(dir, L, static_cast<rsf::MergeMode>(mode));
+    if ((long)m.voxels() > cap) throw rsf::shape_error("rsfref_merge_from_dir: capacity");
+    std::memcpy(out, m.data.data(), m.voxels() * sizeof(float));
+  })
+}
+
 // read_volume (volume_io.cpp:24-113) into out (capacity cap floats).
 int rsfref_read_volume(const char* header, float* out, long cap, int* nx, int* ny, int* nz, float* range2) {
   GUARD({

@@ -25,6 +25,10 @@ from .api import (  # noqa: F401
     write_volume_device,
     plan_tiles,
     run_pipeline,
+    tile_file_name,
+    save_manifest,
+    load_manifest,
+    merge_from_dir_device,
     phantom,
     phantom_device,
     threshold_phi0,

@@ -78,7 +78,7 @@ class rsfg_tile(C.Structure):
 
 class rsfg_pipeline_options(C.Structure):
     _fields_ = [("global_seeding", C.c_int32), ("merge", C.c_int32), ("seed_radius", C.c_double),
-                ("device", C.c_int32), ("fields", C.c_int32)]
+                ("device", C.c_int32), ("fields", C.c_int32), ("spill_dir", C.c_char_p)]
 
 
 class rsfg_phantom_spec(C.Structure):
@@ -171,6 +171,13 @@ SIGNATURES = {
                                     P(rsfg_pipeline_options), FP, FP, C.c_char_p, I32, P(I32)]),
     "rsfg_init_phi_device": (C.c_int, [VP, I32, I32, I32, P(rsfg_blob_params), C.c_double, VP, I32, P(I32),
                                        P(I32), FP, I32, P(I32)]),
+    "rsfg_tile_file_name": (C.c_int, [P(rsfg_tile), C.c_char_p, I32]),
+    "rsfg_save_manifest": (C.c_int, [C.c_char_p, I32, I32, I32, I32, I32, I32, I32, P(rsfg_tile), I32]),
+    "rsfg_load_manifest": (C.c_int, [C.c_char_p, P(I32), P(I32), P(I32), P(rsfg_tile), I32, P(I32)]),
+    "rsfg_merge_from_dir": (C.c_int, [C.c_char_p, I32, I32, I32, I32, I32, I32, I32, P(rsfg_tile), I32, I32, VP,
+                                      I32]),
+    "rsfg_merge_from_dir_host": (C.c_int, [C.c_char_p, I32, I32, I32, I32, I32, I32, I32, P(rsfg_tile), I32, I32,
+                                           FP, I32]),
     "rsfg_init_phi": (C.c_int, [FP, I32, I32, I32, P(rsfg_blob_params), C.c_double, FP, I32, P(I32),
                                 P(I32), FP, I32, P(I32)]),
 }

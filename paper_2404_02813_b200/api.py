@@ -361,9 +361,12 @@ def merge_phi_device(tile_phis, shape, tile_size, curtain, mode="linear", device
 
 
 def run_pipeline(vol, p: "RsfParams", tile_size, *, sigma_b=3.0, response_threshold=0.1, nms_radius=0.0,
-                 dark=False, global_seeding=False, merge="linear", seed_radius=2.0, fields=2, device=0):
+                 dark=False, global_seeding=False, merge="linear", seed_radius=2.0, fields=2, device=0,
+                 spill_dir=None):
     """rsf::run_pipeline (tiling.cpp:201-275) on one GPU: returns (phi, mask,
-    warnings) as host arrays / list of strings."""
+    warnings) as host arrays / list of strings.  spill_dir: every tile's phi
+    is written there (tile_file_name) plus layout.manifest, like the
+    reference's PipelineOptions::spill_dir."""
     vol = np.ascontiguousarray(vol, np.float32)
     nz, ny, nx = vol.shape
     phi = np.empty_like(vol)
@@ -373,6 +376,7 @@ def run_pipeline(vol, p: "RsfParams", tile_size, *, sigma_b=3.0, response_thresh
     L.load().rsfg_pipeline_options_default(C.byref(o))
     o.global_seeding, o.merge, o.seed_radius, o.device, o.fields = (int(global_seeding), MERGE_MODES[merge],
                                                                     seed_radius, device, fields)
+    o.spill_dir = str(spill_dir).encode() if spill_dir else None
     cp = p.to_c()
     warn = C.create_string_buffer(1 << 16)
     nw = C.c_int32()
@@ -380,6 +384,54 @@ def run_pipeline(vol, p: "RsfParams", tile_size, *, sigma_b=3.0, response_thresh
                                      _ptr(phi), _ptr(mask), warn, len(warn), C.byref(nw)))
     lines = [w for w in warn.value.decode().split("\n") if w]
     return phi, mask, lines
+
+
+def _tiles_c(tiles):
+    buf = (L.rsfg_tile * len(tiles))()
+    for b, t in zip(buf, tiles):
+        b.ix, b.iy, b.iz = t["ix"], t["iy"], t["iz"]
+        b.core_origin[:], b.core_extent[:] = t["core_origin"], t["core_extent"]
+        b.pad_origin[:], b.pad_extent[:] = t["pad_origin"], t["pad_extent"]
+    return buf
+
+
+def tile_file_name(tile) -> str:
+    """rsf::tile_file_name (tiling.cpp:195-199)."""
+    buf = C.create_string_buffer(64)
+    check(L.load().rsfg_tile_file_name(_tiles_c([tile]), buf, len(buf)))
+    return buf.value.decode()
+
+
+def save_manifest(path, shape, tile_size, curtain, tiles):
+    """rsf::save_manifest (tiling.cpp:277-295)."""
+    check(L.load().rsfg_save_manifest(str(path).encode(), *shape, *tile_size, curtain, _tiles_c(tiles), len(tiles)))
+
+
+def load_manifest(path):
+    """rsf::load_manifest (tiling.cpp:297-321): (shape, tile_size, curtain,
+    tiles) with tiles as plan_tiles returns them."""
+    d, ts, c, n = (C.c_int32 * 3)(), (C.c_int32 * 3)(), C.c_int32(), C.c_int32()
+    hp = str(path).encode()
+    check(L.load().rsfg_load_manifest(hp, d, ts, C.byref(c), None, 0, C.byref(n)))
+    buf = (L.rsfg_tile * n.value)()
+    check(L.load().rsfg_load_manifest(hp, d, ts, C.byref(c), buf, n.value, C.byref(n)))
+    tiles = [{"ix": t.ix, "iy": t.iy, "iz": t.iz, "core_origin": tuple(t.core_origin),
+              "core_extent": tuple(t.core_extent), "pad_origin": tuple(t.pad_origin),
+              "pad_extent": tuple(t.pad_extent)} for t in buf]
+    return tuple(d), tuple(ts), c.value, tiles
+
+
+def merge_from_dir_device(directory, shape, tile_size, curtain, tiles, mode="linear", device=0):
+    """rsf::merge_from_dir (tiling.cpp:323-332): the spilled tiles are read
+    straight into device buffers and merged on the GPU; returns a torch CUDA
+    tensor (nz, ny, nx)."""
+    import torch
+    nx, ny, nz = shape
+    out = torch.empty((nz, ny, nx), dtype=torch.float32, device=f"cuda:{device}")
+    torch.cuda.synchronize(out.device)
+    check(L.load().rsfg_merge_from_dir(str(directory).encode(), nx, ny, nz, *tile_size, curtain, _tiles_c(tiles),
+                                       len(tiles), MERGE_MODES[mode], out.data_ptr(), device))
+    return out
 
 
 def read_volume_device(header, device=0):

@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -235,6 +237,7 @@ __attribute__((visibility("default"))) void rsfg_pipeline_options_default(rsfg_p
   o->seed_radius = 2.0;
   o->device = 0;
   o->fields = RSFG_FIELDS_2;
+  o->spill_dir = nullptr;
 }
 
 // run_pipeline (tiling.cpp:201-275) on one GPU: host image in, merged phi and
@@ -264,6 +267,8 @@ __attribute__((visibility("default"))) int rsfg_run_pipeline(const float* image,
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return perr(RSFG_ERR_CUDA, "stream");
   const size_t n = (size_t)nx * ny * nz;
+  const bool spill = opt.spill_dir && opt.spill_dir[0];
+  const std::string spill_dir = spill ? opt.spill_dir : "";
   float* d_vol = nullptr;
   float* d_out = nullptr;
   std::vector<float*> tphi(tiles.size(), nullptr);
@@ -366,6 +371,22 @@ __attribute__((visibility("default"))) int rsfg_run_pipeline(const float* image,
       }
     }
     cudaFree(d_tile);
+    // tiling.cpp:256-259: the tile's phi goes to spill_dir as it completes
+    if (rc == RSFG_OK && spill) {
+      if (cudaStreamSynchronize(st) != cudaSuccess) {
+        rc = perr(RSFG_ERR_CUDA, "run_pipeline: CUDA error");
+      } else {
+        const int e = rsfg_write_volume_device((spill_dir + "/" + name).c_str(), tphi[ti], ex, ey, ez, nullptr,
+                                               nullptr, opt.device);
+        if (e) rc = perr(e, rsfg_last_error());
+      }
+    }
+  }
+  // tiling.cpp:262-263: the manifest once every tile is on disk
+  if (rc == RSFG_OK && spill) {
+    const int e = rsfg_save_manifest((spill_dir + "/layout.manifest").c_str(), nx, ny, nz, tx, ty, tz, curtain,
+                                     tiles.data(), (int32_t)tiles.size());
+    if (e) rc = e;
   }
   if (rc == RSFG_OK) {
     if (cudaMalloc(&d_out, n * sizeof(float)) != cudaSuccess) {
@@ -390,6 +411,147 @@ __attribute__((visibility("default"))) int rsfg_run_pipeline(const float* image,
     std::snprintf(warnings, warnings_cap, "%s", all.c_str());
   }
   cleanup();
+  return rc;
+}
+
+__attribute__((visibility("default"))) int rsfg_tile_file_name(const rsfg_tile* t, char* buf, int32_t cap) {
+  if (!t || !buf || cap <= 0) return perr(RSFG_ERR_STATE, "tile_file_name: null buffer");
+  const int k = std::snprintf(buf, cap, "tile_z%02d_y%02d_x%02d.vmh", t->iz, t->iy, t->ix);
+  return k < cap ? RSFG_OK : perr(RSFG_ERR_STATE, "tile_file_name: buffer too small");
+}
+
+// save_manifest (tiling.cpp:277-295): same keys, order and spacing.
+__attribute__((visibility("default"))) int rsfg_save_manifest(const char* path, int32_t nx, int32_t ny, int32_t nz,
+                                                              int32_t tx, int32_t ty, int32_t tz, int32_t curtain,
+                                                              const rsfg_tile* tiles, int32_t n_tiles) {
+  const std::string ps = path ? path : "";
+  std::ofstream out(ps, std::ios::trunc);
+  if (!out) return perr(RSFG_ERR_IO, "cannot write manifest: " + ps);
+  out << "dims: " << nx << " " << ny << " " << nz << "\n";
+  out << "tile_size: " << tx << " " << ty << " " << tz << "\n";
+  out << "curtain: " << curtain << "\n";
+  for (int32_t i = 0; i < n_tiles; ++i) {
+    const rsfg_tile& t = tiles[i];
+    out << "tile: " << t.ix << " " << t.iy << " " << t.iz;
+    for (const int32_t* a : {t.core_origin, t.core_extent, t.pad_origin, t.pad_extent})
+      out << " " << a[0] << " " << a[1] << " " << a[2];
+    out << "\n";
+  }
+  if (!out) return perr(RSFG_ERR_IO, "short write to manifest: " + ps);
+  return RSFG_OK;
+}
+
+namespace {
+int load_manifest(const std::string& ps, int32_t* dims3, int32_t* tile3, int32_t* curtain,
+                  std::vector<rsfg_tile>& tiles) {
+  std::ifstream in(ps);
+  if (!in) return perr(RSFG_ERR_IO, "cannot open manifest: " + ps);
+  int d[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, c = 0;
+  std::string line;
+  while (std::getline(in, line)) {  // tiling.cpp:297-321
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ls(line);
+    std::string key;
+    ls >> key;
+    if (key == "dims:") {
+      ls >> d[0] >> d[1] >> d[2];
+    } else if (key == "tile_size:") {
+      ls >> ts[0] >> ts[1] >> ts[2];
+    } else if (key == "curtain:") {
+      ls >> c;
+    } else if (key == "tile:") {
+      rsfg_tile t;
+      ls >> t.ix >> t.iy >> t.iz;
+      for (int32_t* a : {t.core_origin, t.core_extent, t.pad_origin, t.pad_extent}) ls >> a[0] >> a[1] >> a[2];
+      tiles.push_back(t);
+    } else {
+      return perr(RSFG_ERR_IO, "unknown manifest key '" + key + "' in " + ps);
+    }
+    if (!ls) return perr(RSFG_ERR_IO, "garbled manifest line in " + ps + ": " + line);
+  }
+  if (tiles.empty()) return perr(RSFG_ERR_IO, "manifest has no tiles: " + ps);
+  for (int k = 0; k < 3; ++k) {
+    if (dims3) dims3[k] = d[k];
+    if (tile3) tile3[k] = ts[k];
+  }
+  if (curtain) *curtain = c;
+  return RSFG_OK;
+}
+}  // namespace
+
+__attribute__((visibility("default"))) int rsfg_load_manifest(const char* path, int32_t* dims3, int32_t* tile_size3,
+                                                              int32_t* curtain, rsfg_tile* tiles, int32_t cap,
+                                                              int32_t* n_tiles) {
+  std::vector<rsfg_tile> v;
+  if (int rc = load_manifest(path ? path : "", dims3, tile_size3, curtain, v)) return rc;
+  if (n_tiles) *n_tiles = (int32_t)v.size();
+  for (size_t i = 0; tiles && i < v.size() && (int32_t)i < cap; ++i) tiles[i] = v[i];
+  return RSFG_OK;
+}
+
+// merge_from_dir (tiling.cpp:323-332): each tile file is read straight into a
+// device buffer (rsfg_read_volume_device), then one device merge.
+__attribute__((visibility("default"))) int rsfg_merge_from_dir(const char* dir, int32_t nx, int32_t ny, int32_t nz,
+                                                               int32_t tx, int32_t ty, int32_t tz, int32_t curtain,
+                                                               const rsfg_tile* layout_tiles, int32_t n_tiles,
+                                                               int32_t mode, float* d_out, int32_t device) {
+  if (!dir || !layout_tiles || !d_out) return perr(RSFG_ERR_STATE, "merge_from_dir: null argument");
+  if (mode < 0 || mode > 3) return perr(RSFG_ERR_PARAM, "merge_phi: unknown mode");
+  const int32_t d[3] = {nx, ny, nz}, ts[3] = {tx, ty, tz};
+  const std::vector<rsfg_tile> tiles(layout_tiles, layout_tiles + std::max(n_tiles, 0));
+  if (cudaSetDevice(device) != cudaSuccess) return perr(RSFG_ERR_CUDA, "merge_from_dir: bad device");
+  std::vector<float*> tphi(tiles.size(), nullptr);
+  int rc = RSFG_OK;
+  for (size_t i = 0; i < tiles.size() && !rc; ++i) {
+    const rsfg_tile& t = tiles[i];
+    const int64_t tn = (int64_t)t.pad_extent[0] * t.pad_extent[1] * t.pad_extent[2];
+    char name[64];
+    rsfg_tile_file_name(&t, name, sizeof name);
+    const std::string hp = std::string(dir) + "/" + name;
+    int32_t fx = 0, fy = 0, fz = 0, eb = 0;
+    double sp[3];
+    if ((rc = rsfg_volume_info(hp.c_str(), &fx, &fy, &fz, sp, &eb))) break;
+    if (fx != t.pad_extent[0] || fy != t.pad_extent[1] || fz != t.pad_extent[2]) {
+      rc = perr(RSFG_ERR_SHAPE, "merge_phi: tile " + std::string(name) + " dims do not match its box");
+      break;
+    }
+    if (cudaMalloc(&tphi[i], tn * sizeof(float)) != cudaSuccess) {
+      rc = perr(RSFG_ERR_OOM, "merge_from_dir: out of device memory");
+      break;
+    }
+    rc = rsfg_read_volume_device(hp.c_str(), tphi[i], tn, device, nullptr, nullptr);
+  }
+  if (!rc) {
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+      rc = perr(RSFG_ERR_CUDA, "stream");
+    } else {
+      rc = merge_device(tphi.data(), (int)tphi.size(), d[0], d[1], d[2], ts[0], ts[1], ts[2], curtain, mode, d_out,
+                        st);
+      cudaStreamDestroy(st);
+    }
+  }
+  for (float* q : tphi) cudaFree(q);
+  return rc;
+}
+
+// Same with a HOST output buffer (the reference's merge_from_dir returns a
+// host Volume): merged on the device, one D2H.
+__attribute__((visibility("default"))) int rsfg_merge_from_dir_host(const char* dir, int32_t nx, int32_t ny,
+                                                                    int32_t nz, int32_t tx, int32_t ty, int32_t tz,
+                                                                    int32_t curtain, const rsfg_tile* tiles,
+                                                                    int32_t n_tiles, int32_t mode, float* out,
+                                                                    int32_t device) {
+  if (!out) return perr(RSFG_ERR_STATE, "merge_from_dir: null argument");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return perr(RSFG_ERR_SHAPE, "merge_from_dir: bad volume dims");
+  if (cudaSetDevice(device) != cudaSuccess) return perr(RSFG_ERR_CUDA, "merge_from_dir: bad device");
+  const size_t bytes = (size_t)nx * ny * nz * sizeof(float);
+  float* d_out = nullptr;
+  if (cudaMalloc(&d_out, bytes) != cudaSuccess) return perr(RSFG_ERR_OOM, "merge_from_dir: out of device memory");
+  int rc = rsfg_merge_from_dir(dir, nx, ny, nz, tx, ty, tz, curtain, tiles, n_tiles, mode, d_out, device);
+  if (!rc && cudaMemcpy(out, d_out, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = perr(RSFG_ERR_CUDA, "merge_from_dir: CUDA error");
+  cudaFree(d_out);
   return rc;
 }
 

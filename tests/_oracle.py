@@ -260,6 +260,17 @@ class RefLib:
                                                  int(global_seeding), mode, seed_radius, phi, mask, C.byref(nw)))
         return phi, mask, nw.value
 
+    def save_manifest(self, path, shape, tile_size, sigma1, sigma2=0.0):
+        self._check(self.lib.rsfref_save_manifest(str(path).encode(), *shape, *tile_size, C.c_double(sigma1),
+                                                  C.c_double(sigma2)))
+
+    def merge_from_dir(self, directory, manifest, shape, mode=0):
+        nx, ny, nz = shape
+        out = np.empty((nz, ny, nx), np.float32)
+        self._check(self.lib.rsfref_merge_from_dir(str(directory).encode(), str(manifest).encode(), mode,
+                                                   out.ctypes.data_as(C.POINTER(C.c_float)), C.c_long(out.size)))
+        return out
+
     def read_volume(self, header, cap=1 << 26):
         out = np.empty(cap, np.float32)
         nx, ny, nz = C.c_int(), C.c_int(), C.c_int()

@@ -1,8 +1,8 @@
 // Drives include/rsfgpu.hpp (the reference-shaped C++ surface) the way a
 // reference caller would: rsf::evolve, init_phi, plan_tiles, run_pipeline
-// (rsf.hpp:97-101, seeding.hpp:60-61, tiling.hpp:28-60) with the namespace
+// (rsf.hpp:97-101, seeding.hpp:60-61, tiling.hpp:28-71) with the namespace
 // switched to rsfgpu.  Used by tests/test_cpp_wrapper.py.
-//   wrapper_check cpu                      exceptions + plan_tiles, no GPU
+//   wrapper_check cpu [dir]                exceptions, plan_tiles, manifest; no GPU
 //   wrapper_check gpu nx ny nz image out   evolve / init_phi / run_pipeline
 #include <cstdio>
 #include <fstream>
@@ -36,7 +36,17 @@ int main(int argc, char** argv) {
     const bool e2 = throws<rsfgpu::param_error>(
         [&] { rsfgpu::plan_tiles({64, 64, 64}, {8, 8, 8}, 3.0, 0.0); }, "");
     const rsfgpu::TileLayout L = rsfgpu::plan_tiles({100, 80, 60}, {48, 40, 30}, 2.0, 1.0);
-    std::printf("{\"param_error\": %d, \"tile_error\": %d, \"curtain\": %d, \"tiles\": [", e1, e2, L.curtain);
+    const std::string mf = argc > 2 ? std::string(argv[2]) + "/layout.manifest" : "layout.manifest";
+    rsfgpu::save_manifest(mf, L);
+    const rsfgpu::TileLayout B = rsfgpu::load_manifest(mf);
+    bool same = B.curtain == L.curtain && B.vol_dims == L.vol_dims && B.tile_size == L.tile_size &&
+                B.tiles.size() == L.tiles.size();
+    for (std::size_t i = 0; same && i < B.tiles.size(); ++i)
+      same = B.tiles[i].pad_extent == L.tiles[i].pad_extent && B.tiles[i].core_origin == L.tiles[i].core_origin;
+    const bool e3 = throws<rsfgpu::io_error>([&] { rsfgpu::load_manifest(mf + ".missing"); }, "cannot open manifest");
+    std::printf("{\"manifest_roundtrip\": %d, \"io_error\": %d, \"last_name\": \"%s\", ", same, e3,
+                rsfgpu::tile_file_name(L.tiles.back()).c_str());
+    std::printf("\"param_error\": %d, \"tile_error\": %d, \"curtain\": %d, \"tiles\": [", e1, e2, L.curtain);
     for (std::size_t i = 0; i < L.tiles.size(); ++i) {
       const rsfgpu::TileBox& t = L.tiles[i];
       std::printf("%s[%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d]", i ? "," : "", t.ix, t.iy, t.iz,
@@ -66,9 +76,13 @@ int main(int argc, char** argv) {
   dump(out + "/mask.raw", rsfgpu::extract_mask(phi));
 
   const rsfgpu::TileLayout L = rsfgpu::plan_tiles(img.dims, {nx / 2, ny / 2, nz / 2}, p.sigma1, p.sigma2);
-  const rsfgpu::PipelineResult r = rsfgpu::run_pipeline(img, p, bp, L, 4);
+  rsfgpu::PipelineOptions po;
+  po.spill_dir = out;  // tiles + layout.manifest next to the other outputs
+  const rsfgpu::PipelineResult r = rsfgpu::run_pipeline(img, p, bp, L, 4, po);
   dump(out + "/pipe_phi.raw", r.phi);
   dump(out + "/pipe_mask.raw", r.mask);
+  const rsfgpu::TileLayout back = rsfgpu::load_manifest(out + "/layout.manifest");
+  dump(out + "/merged_from_dir.raw", rsfgpu::merge_from_dir(out, back));
 
   std::printf("{\"n_seeds\": %zu, \"seed0\": [%d, %d, %d, %.9g], \"n_tiles\": %zu, \"n_warnings\": %zu}\n",
               seeds.points.size(), seeds.points.empty() ? -1 : seeds.points[0].x,

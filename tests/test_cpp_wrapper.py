@@ -28,10 +28,12 @@ def wrapper_bin(tmp_path_factory):
     return out
 
 
-def test_cpp_wrapper_host_logic(wrapper_bin):
+def test_cpp_wrapper_host_logic(wrapper_bin, tmp_path):
     import paper_2404_02813_b200 as rsf
-    r = json.loads(subprocess.run([str(wrapper_bin), "cpu"], check=True, capture_output=True, text=True).stdout)
+    r = json.loads(subprocess.run([str(wrapper_bin), "cpu", str(tmp_path)], check=True, capture_output=True,
+                                  text=True).stdout)
     assert r["param_error"] == 1 and r["tile_error"] == 1
+    assert r["manifest_roundtrip"] == 1 and r["io_error"] == 1 and r["last_name"] == "tile_z01_y01_x02.vmh"
     tiles, curtain = rsf.plan_tiles((100, 80, 60), (48, 40, 30), 2.0, 1.0)
     assert r["curtain"] == curtain
     want = [[t["ix"], t["iy"], t["iz"], *t["core_origin"], *t["core_extent"], *t["pad_origin"], *t["pad_extent"]]
@@ -69,3 +71,5 @@ def test_cpp_wrapper_gpu_matches_api(wrapper_bin, tmp_path, ref):
     assert r["n_tiles"] == 8 and r["n_warnings"] == len(warn)
     assert np.array_equal(load("pipe_phi.raw"), phi_p)
     assert np.array_equal(load("pipe_mask.raw"), mask_p)
+    assert np.array_equal(load("merged_from_dir.raw"), phi_p)  # spill_dir + load_manifest + merge_from_dir
+    assert (tmp_path / "layout.manifest").exists() and len(list(tmp_path.glob("tile_z*.vmh"))) == 8

@@ -50,3 +50,30 @@ def test_plan_tiles_errors():
         rsf.plan_tiles((64, 64, 64), (16, 16, 16), 3.0)
     with pytest.raises(rsf.ShapeError, match="bad volume dims"):
         rsf.plan_tiles((0, 64, 64), (32, 32, 32), 1.0)
+
+
+def test_run_pipeline_spill_and_merge_from_dir(ref, tmp_path):
+    """PipelineOptions::spill_dir (tiling.cpp:256-263) and merge_from_dir
+    (tiling.cpp:323-332): every tile lands under its tile_file_name plus the
+    reference's manifest; the reference's own load_manifest + merge_from_dir
+    over our spill directory, and ours on the device, both reproduce the
+    returned phi bit for bit."""
+    import paper_2404_02813_b200 as rsf
+    img, _, _ = case(80, 64, 48, n_branches=6, init="threshold")
+    img = np.ascontiguousarray(img)
+    shape, tile = (80, 64, 48), (40, 32, 24)
+    p = rsf.RsfParams(sigma1=2.0, max_iters=10)
+    for mode in ("linear", "average"):
+        d = tmp_path / mode
+        d.mkdir()
+        phi, mask, _ = rsf.run_pipeline(img, p, tile, merge=mode, spill_dir=d)
+        tiles, curtain = rsf.plan_tiles(shape, tile, 2.0)
+        assert sorted(f.name for f in d.glob("*.vmh")) == sorted(rsf.tile_file_name(t) for t in tiles)
+        ref.save_manifest(tmp_path / "ref.manifest", shape, tile, 2.0)
+        assert (d / "layout.manifest").read_bytes() == (tmp_path / "ref.manifest").read_bytes()
+        got = rsf.merge_from_dir_device(d, shape, tile, curtain, tiles, mode).cpu().numpy()
+        assert np.array_equal(got, phi)
+        want = ref.merge_from_dir(d, d / "layout.manifest", shape, rsf.api.MERGE_MODES[mode])
+        assert np.array_equal(want, phi)
+    with pytest.raises(rsf.VolumeIOError, match="cannot write"):
+        rsf.run_pipeline(img, p, tile, spill_dir=tmp_path / "no" / "such" / "dir")
