@@ -880,8 +880,8 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
   struct SideGuard {
     cudaStream_t* st;
     cudaEvent_t* e;
-    ~SideGuard() {
-      if (*st) cudaStreamDestroy(*st);
+    ~SideGuard() {  // on every return path the copy from the caller's buffer is finished
+      if (*st) cudaStreamSynchronize(*st), cudaStreamDestroy(*st);
       if (*e) cudaEventDestroy(*e);
     }
   } side_guard{&side, &phi_up};
