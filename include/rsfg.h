@@ -67,9 +67,10 @@ typedef struct rsfg_options {
   int32_t fields;      /* RSFG_FIELDS_2 or RSFG_FIELDS_4 (default: RSFG_FIELDS_2)      */
   int32_t check_every; /* evolve/run: host checks blowup every N steps (default 25)     */
   int32_t use_graphs;  /* reserved: per-step launches are plain stream launches          */
-  int32_t reuse_workspace; /* rsfg_evolve keeps its device buffers for the calling thread's
-                              next call of the same shape (default 1); see
-                              rsfg_release_workspace()                                  */
+  int32_t reuse_workspace; /* opt-in (default 0): rsfg_evolve keeps its device buffers
+                              (~32 B/voxel) for the calling thread's next call of the
+                              same shape; freed by rsfg_release_workspace(), by a call
+                              with reuse_workspace = 0, or when the thread exits       */
   int32_t reserved[3];
 } rsfg_options;
 

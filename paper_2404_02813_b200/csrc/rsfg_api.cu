@@ -125,6 +125,7 @@ struct rsfg_slab {
   float2* hh = nullptr;
   bool hh_mode = false;
   bool hh_valid = false;
+  std::string env_key;  // kernel-variant environment at setup (workspace reuse must match it)
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -151,7 +152,30 @@ struct rsfg_state {
 };
 
 namespace {
-thread_local rsfg_state* t_cache = nullptr;  // rsfg_evolve workspace of this thread
+void destroy_state(rsfg_state* st);
+// rsfg_evolve workspace of this thread (opt-in, rsfg_options.reuse_workspace):
+// freed by rsfg_release_workspace() or when the thread exits.
+struct WorkspaceCache {
+  rsfg_state* st = nullptr;
+  ~WorkspaceCache() {
+    if (st) destroy_state(st);
+  }
+};
+thread_local WorkspaceCache t_cache;
+
+// Environment switches that select kernel variants at setup (tests and
+// probes flip them); a reused workspace must have been set up under the same.
+std::string variant_env_key() {
+  std::string k;
+  for (const char* v : {"RSFG_HH", "RSFG_XY2", "RSFG_XY2_TY", "RSFG_TMA", "RSFG_ZST4", "RSFG_FUSED"}) {
+    const char* e = std::getenv(v);
+    k += v;
+    k += '=';
+    k += e ? e : "";
+    k += ';';
+  }
+  return k;
+}
 }
 
 namespace {
@@ -172,6 +196,12 @@ void release(rsfg_slab* s) {
   cudaFree(s->mm);
   if (s->h_counters) cudaFreeHost(s->h_counters);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+void destroy_state(rsfg_state* st) {
+  if (!st) return;
+  release(&st->e);
+  delete st;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -304,6 +334,7 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   s->tid.w[0] = 1.0f;
   s->tid.r = 0;
   s->fast = rsfg::has_fast_radius(s->t1.r);
+  s->env_key = variant_env_key();
   s->nx = nx;
   s->ny = ny;
   s->nz = nz;
@@ -604,7 +635,7 @@ __attribute__((visibility("default"))) void rsfg_options_default(rsfg_options* o
   o->fields = RSFG_FIELDS_2;
   o->check_every = 25;
   o->use_graphs = 1;
-  o->reuse_workspace = 1;
+  o->reuse_workspace = 0;
 }
 
 __attribute__((visibility("default"))) int rsfg_params_validate(const rsfg_params* p) { return validate(p); }
@@ -803,11 +834,7 @@ __attribute__((visibility("default"))) int rsfg_state_variant(const rsfg_state* 
   return RSFG_OK;
 }
 
-__attribute__((visibility("default"))) void rsfg_state_destroy(rsfg_state* st) {
-  if (!st) return;
-  release(&st->e);
-  delete st;
-}
+__attribute__((visibility("default"))) void rsfg_state_destroy(rsfg_state* st) { destroy_state(st); }
 
 // ------------------------------------------------------------------ evolve
 namespace {
@@ -835,19 +862,23 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
   // thread and serve the next call of the same shape/radii (no cudaMalloc,
   // stream or pinned-buffer setup on the hot e2e path).
   rsfg_state* st = nullptr;
-  if (opt.reuse_workspace && t_cache) {
-    rsfg_slab* c = &t_cache->e;
+  if (t_cache.st && !opt.reuse_workspace) {  // opt-out frees a kept workspace
+    rsfg_state_destroy(t_cache.st);
+    t_cache.st = nullptr;
+  }
+  if (opt.reuse_workspace && t_cache.st) {
+    rsfg_slab* c = &t_cache.st->e;
     if (c->dev == opt.device && c->nx == nx && c->ny == ny && c->nz == nz && c->fields == opt.fields &&
-        c->p.sigma1 == p->sigma1 && c->p.sigma2 == p->sigma2) {
-      st = t_cache;
-      t_cache = nullptr;
+        c->p.sigma1 == p->sigma1 && c->p.sigma2 == p->sigma2 && c->env_key == variant_env_key()) {
+      st = t_cache.st;
+      t_cache.st = nullptr;
       if (int rc = reconfigure(c, p, &opt)) {
         rsfg_state_destroy(st);
         return rc;
       }
     } else {
-      rsfg_state_destroy(t_cache);
-      t_cache = nullptr;
+      rsfg_state_destroy(t_cache.st);
+      t_cache.st = nullptr;
     }
   }
   if (!st) {
@@ -864,8 +895,8 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
     bool keep;
     ~StGuard() {
       if (keep && st->e.valid) {
-        if (t_cache) rsfg_state_destroy(t_cache);
-        t_cache = st;
+        if (t_cache.st) rsfg_state_destroy(t_cache.st);
+        t_cache.st = st;
       } else {
         rsfg_state_destroy(st);
       }
@@ -987,8 +1018,8 @@ __attribute__((visibility("default"))) int rsfg_evolve(const float* image, float
 }
 
 __attribute__((visibility("default"))) void rsfg_release_workspace(void) {
-  rsfg_state_destroy(t_cache);
-  t_cache = nullptr;
+  rsfg_state_destroy(t_cache.st);
+  t_cache.st = nullptr;
 }
 
 __attribute__((visibility("default"))) int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device) {

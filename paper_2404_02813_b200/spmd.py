@@ -21,7 +21,13 @@ import ctypes as C
 import numpy as np
 
 from . import _lib as L
-from .api import RsfParams, check, gaussian_kernel, options
+from .api import BlowupError, RsfParams, check, gaussian_kernel, options
+
+
+def blowup_message(first_bad: int, nx: int, ny: int, iteration: int) -> str:
+    """rsf::blowup_error text (rsf.cpp:346-352) for a global voxel index."""
+    x, y, z = first_bad % nx, (first_bad // nx) % ny, first_bad // (nx * ny)
+    return f"evolution produced a non-finite value at voxel ({x},{y},{z}), iteration {iteration}"
 
 
 def halo_width(p: RsfParams) -> int:
@@ -63,8 +69,12 @@ class Slab:
         """Takes the FULL volumes (numpy host arrays, or torch CUDA tensors on
         the slab's device) and uploads the held planes [zb, ze)."""
         if hasattr(phi_vol, "data_ptr"):  # torch CUDA tensors: device-to-device
+            import torch
             ph = phi_vol[self.zb:self.ze].contiguous()
             im = img_vol[self.zb:self.ze].contiguous()
+            # the slab copies on its own non-blocking stream: the producers of
+            # these tensors (torch's stream) must be done first
+            torch.cuda.synchronize(ph.device)
             check(self.lib.rsfg_slab_upload_device(self.h, ph.data_ptr(), im.data_ptr()))
             return
         ph = np.ascontiguousarray(phi_vol[self.zb:self.ze], np.float32)
@@ -121,8 +131,11 @@ class Slab:
 class SlabSet:
     """P slabs in one process (one or several local GPUs)."""
 
-    def __init__(self, phi0, I, p: RsfParams, parts: int, *, fields=2, devices=None):
+    def __init__(self, phi0, I, p: RsfParams, parts: int, *, fields=2, devices=None, check_every=25):
         nz, ny, nx = phi0.shape
+        self.nx, self.ny = nx, ny
+        self.check_every = max(1, check_every)
+        self.iteration = 0
         self.halo = halo_width(p)
         self.ranges = plan_slabs(nz, parts, self.halo)
         devices = devices or [0] * parts
@@ -143,6 +156,18 @@ class SlabSet:
             check(lib.rsfg_slab_exchange(a.h, b.h))
         for s in self.slabs:
             s.step_finish()
+        self.iteration += 1
+        if self.iteration % self.check_every == 0:
+            self.check_blowup()
+
+    def check_blowup(self):
+        """Raises BlowupError (rsf.cpp:346-352) if the LAST step produced a
+        non-finite phi anywhere (smallest global voxel index).  A non-finite
+        value spreads to every later step, so checking every check_every steps
+        finds it; the reported iteration is the one checked."""
+        bads = [b for b in (s.counters()[1] for s in self.slabs) if b >= 0]
+        if bads:
+            raise BlowupError(blowup_message(min(bads), self.nx, self.ny, self.iteration))
 
     def sign_changes(self) -> int:
         return sum(s.counters()[0] for s in self.slabs)
@@ -191,13 +216,17 @@ class DistSlab:
     lets several ranks share one GPU, which is how this path is tested on
     single-GPU machines (tests/test_gpu_distslab.py)."""
 
-    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None, transport="device"):
+    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None, transport="device",
+                 check_every=25):
         import torch
+        self.check_every = max(1, check_every)
+        self.iteration = 0
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.rank = dist.get_rank() if rank is None else rank
         self.world = dist.get_world_size() if world is None else world
         nz, ny, nx = phi0.shape
+        self.nx, self.ny = nx, ny
         self.halo = halo_width(p)
         self.ranges = plan_slabs(nz, self.world, self.halo)
         z0, z1 = self.ranges[self.rank]
@@ -221,12 +250,29 @@ class DistSlab:
 
     def step(self):
         if self.transport == "host":
-            return self._step_host()
-        reqs = start_halo_exchange(self.dist, self.rank, self.world, self._views(0), self._views(1))
-        self.slab.step_interior()  # overlaps the exchange (no halo needed)
-        for q in reqs:
-            q.wait()
-        self.slab.step_finish()
+            self._step_host()
+        else:
+            reqs = start_halo_exchange(self.dist, self.rank, self.world, self._views(0), self._views(1))
+            self.slab.step_interior()  # overlaps the exchange (no halo needed)
+            for q in reqs:
+                q.wait()
+            self.slab.step_finish()
+        self.iteration += 1
+        if self.iteration % self.check_every == 0:
+            self.check_blowup()
+
+    def check_blowup(self):
+        """Global first non-finite voxel of the last step (MIN over ranks of each
+        slab's first bad index, rsf.cpp:346-352); raises BlowupError on every rank."""
+        t = self.torch
+        _, bad = self.slab.counters()
+        big = t.iinfo(t.int64).max
+        v = t.tensor([bad if bad >= 0 else big], dtype=t.int64,
+                     device="cuda" if self.transport == "device" else "cpu")
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN)
+        g = int(v.item())
+        if g != big:
+            raise BlowupError(blowup_message(g, self.nx, self.ny, self.iteration))
 
     def _step_host(self):
         self.stream.synchronize()  # the previous step's phi is complete

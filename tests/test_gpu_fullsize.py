@@ -27,20 +27,44 @@ def inputs():
     return img, np.ascontiguousarray(phi, np.float32)
 
 
-def test_fullsize_one_step_vs_reference(ref, inputs):
+@pytest.mark.parametrize("sigma1", [3.0, 6.0])  # cfg 2 (R = 9) and cfg 3 (R = 18)
+def test_fullsize_one_step_vs_reference(ref, inputs, sigma1):
     import paper_2404_02813_b200 as rsf
     from _oracle import params
     img, phi = inputs
     ref.set_workers(0)
-    rs = ref.state(phi, img, params(sigma1=3.0))
+    rs = ref.state(phi, img, params(sigma1=sigma1))
     frac_r = rs.step()
     want = rs.phi()
-    st = rsf.init_evolution(phi, img, rsf.RsfParams(sigma1=3.0))
+    st = rsf.init_evolution(phi, img, rsf.RsfParams(sigma1=sigma1))
     frac_g = st.step()
     got = st.phi
-    err = np.abs(got.astype(np.float64) - want) / np.maximum(1.0, np.abs(want))
+    d = np.abs(got.astype(np.float64) - want)
+    assert float(d.max()) <= 1e-4, float(d.max())  # SURVEY 8(c) P1, absolute
+    err = d / np.maximum(1.0, np.abs(want))
     assert float(err.max()) <= 1e-4, float(err.max())
     assert abs(frac_g - frac_r) * img.size <= max(2, 1e-5 * img.size)
+
+
+@pytest.mark.slow
+def test_fullsize_threshold_P3(ref, inputs):
+    """The bench's own workload (cfg 2: 512^3, sigma1 = 3, threshold phi0)
+    over a bounded run: 10 iterations on the GPU and in the compiled
+    reference (all host cores), mask statistics of SURVEY.md 8(c) P3."""
+    import paper_2404_02813_b200 as rsf
+    from _oracle import params
+    img, _ = inputs
+    phi0 = rsf.threshold_phi0(img)
+    iters = 10
+    ref.set_workers(0)
+    want = ref.evolve(phi0, img, params(sigma1=3.0, max_iters=iters))
+    got = rsf.evolve(phi0, img, rsf.RsfParams(sigma1=3.0, max_iters=iters))
+    m_ref, m_got = want < 0, got < 0
+    mismatch = int(np.count_nonzero(m_ref != m_got))
+    assert mismatch <= 1e-5 * img.size, mismatch
+    assert rsf.dice(m_got, m_ref) >= 0.9999
+    close = np.abs(got.astype(np.float64) - want) <= 1e-3 + 1e-4 * np.abs(want)
+    assert close.mean() >= 0.995, close.mean()
 
 
 def test_fullsize_properties(inputs, monkeypatch):
