@@ -71,8 +71,24 @@ typedef struct rsfg_options {
                               (~32 B/voxel) for the calling thread's next call of the
                               same shape; freed by rsfg_release_workspace(), by a call
                               with reuse_workspace = 0, or when the thread exits       */
-  int32_t reserved[3];
+  int32_t profile_stages;  /* rsfg_evolve: fill rsfg_report.stage_seconds (KernelProfile,
+                              rsf.hpp:64-69) from per-kernel CUDA events (default 0)   */
+  int32_t reserved[2];
 } rsfg_options;
+
+/* The reference's per-iteration stage rows (rsf::KernelProfile::names(),
+ * rsf.cpp:228-233), in its order: "H-I", "H+I", "K*H-I", "K*H+I", "K*H-",
+ * "K*H+", "delta", "grad", "grad-mag", "laplacian", "grad/|grad|",
+ * "R-combine", "E+", "E-".  The kernels here fuse them, so each kernel's
+ * CUDA-event time is booked on ONE row and the rows fused into it read 0:
+ *   row 0  "H-I"       the stand-alone Heaviside pass (pairs kernel 1 reads in
+ *                      the stored-Heaviside mode, halo planes);
+ *   row 2  "K*H-I"     kernel 1: Heaviside (unless stored) + y and x passes of
+ *                      the (H, H I) pairs (generic radii: all three passes);
+ *   row 11 "R-combine" kernel 2: z pass, region means r+-, F- - F+, delta,
+ *                      grad, grad/|grad|, div, Laplacian, combine, update.
+ * rsfg_stage_carrier(i) gives the row that carries stage i's time. */
+#define RSFG_STAGE_COUNT 14
 
 typedef struct rsfg_report {
   int32_t iterations;             /* steps completed                                  */
@@ -81,6 +97,7 @@ typedef struct rsfg_report {
   double last_sign_change_fraction;
   double ms_h2d, ms_init, ms_loop, ms_d2h; /* CUDA-event timings of the call's phases    */
   int64_t gpu_launches;           /* kernels launched by the call                     */
+  double stage_seconds[RSFG_STAGE_COUNT]; /* options.profile_stages: per-row kernel time */
 } rsfg_report;
 
 /* Called every stop_every iterations with the current phi (host copy);
@@ -135,6 +152,18 @@ int rsfg_state_energy(rsfg_state* s, float* E_host); /* energy() (rsf.cpp:315-32
 #define RSFG_PROFILE_COUNT 2
 int rsfg_state_profile(rsfg_state* s, int32_t steps, double* ms);
 const char* rsfg_profile_name(int32_t i);
+/* Stage-row names (RSFG_STAGE_COUNT, the reference's) and the row carrying
+ * each stage's time in this implementation (see RSFG_STAGE_COUNT). */
+const char* rsfg_stage_name(int32_t i);
+int32_t rsfg_stage_carrier(int32_t i);
+/* evolve_step with a KernelProfile (rsf.cpp:324-357 with StageTimer,
+ * rsf.cpp:36-70): one step; ADDS each row's CUDA-event seconds to
+ * stage_seconds[0..RSFG_STAGE_COUNT). */
+int rsfg_state_step_profiled(rsfg_state* s, double* sign_change_fraction, double* stage_seconds);
+/* New step parameters for an existing state (evolve_step takes p on every
+ * call): epsilon, alpha, beta, dt, floors, convergence_fraction, max_iters.
+ * sigma1/sigma2 stay the state's own (its kernels, rsf.cpp:299-300). */
+int rsfg_state_set_params(rsfg_state* s, const rsfg_params* p);
 int rsfg_state_read_phi(rsfg_state* s, float* phi_host);
 int rsfg_state_write_phi(rsfg_state* s, const float* phi_host);
 int rsfg_state_mask(rsfg_state* s, float* mask_host);
@@ -153,6 +182,23 @@ int64_t rsfg_state_launches(const rsfg_state* s);
 int rsfg_state_variant(const rsfg_state* s, int32_t* flags, int32_t* xy_bytes_per_voxel,
                        int32_t* zst_bytes_per_voxel);
 void rsfg_state_destroy(rsfg_state* s);
+
+/* ---- term-level APIs (rsf.hpp:39-50; rsf.cpp:235-291) ---------------------
+ * region_intensities: r+- = clamp(K*(H+- I) / max(K*H+-, denom_floor), min I,
+ * max I) with K the sigma1 Gaussian, H+ = heaviside_eps(phi), H- = 1 - H+.
+ * directional_forces: F+- = (KI2 - 2 r+- KI) + r+-^2 (f64, rounded to f32).
+ * Errors as rsf::param_error (epsilon/denom_floor) / shape_error. */
+int rsfg_region_intensities(const float* image, const float* phi, int32_t nx, int32_t ny, int32_t nz,
+                            double sigma1, double epsilon, double denom_floor, float* r_plus, float* r_minus,
+                            int32_t device);
+int rsfg_region_intensities_device(const float* d_image, const float* d_phi, int32_t nx, int32_t ny, int32_t nz,
+                                   double sigma1, double epsilon, double denom_floor, float* d_r_plus,
+                                   float* d_r_minus, int32_t device);
+int rsfg_directional_forces(const float* r_plus, const float* r_minus, const float* ki, const float* ki2, int64_t n,
+                            float* f_plus, float* f_minus, int32_t device);
+int rsfg_directional_forces_device(const float* d_r_plus, const float* d_r_minus, const float* d_ki,
+                                   const float* d_ki2, int64_t n, float* d_f_plus, float* d_f_minus,
+                                   int32_t device);
 
 /* ---- z-slab SPMD primitives (multi-GPU) -------------------
  * A slab owns global planes [z0, z1) of an nx*ny*nz volume and holds

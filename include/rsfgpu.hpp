@@ -8,6 +8,8 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
+#include <cstddef>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -102,13 +104,70 @@ inline void check_same_dims(const Volume& a, const Volume& b, const char* what) 
                       std::to_string(b.dims.nz));
 }
 
-// rsf::evolve (rsf.hpp:97-98).  `options` selects the device and the
-// convolution form (RSFG_FIELDS_2 default, RSFG_FIELDS_4 reference form).
+inline std::string to_string(const Dims& d) {  // core.hpp:46-48
+  return std::to_string(d.nx) + "x" + std::to_string(d.ny) + "x" + std::to_string(d.nz);
+}
+
+// rsf::replicate_z / take_slice_z (volume.hpp:78-79, volume.cpp:47-67).
+inline Volume replicate_z(const Volume& v) {
+  if (v.dims.nz != 1) throw shape_error("replicate_z: expects nz == 1");
+  Volume out(v.dims.nx, v.dims.ny, 2);
+  std::copy(v.data.begin(), v.data.end(), out.data.begin());
+  std::copy(v.data.begin(), v.data.end(), out.data.begin() + (std::ptrdiff_t)v.voxels());
+  return out;
+}
+inline Volume take_slice_z(const Volume& v, int z) {
+  if (z < 0 || z >= v.dims.nz) throw shape_error("take_slice_z: z out of range");
+  Volume out(v.dims.nx, v.dims.ny, 1);
+  const std::size_t n = out.voxels();
+  std::copy(v.data.begin() + (std::ptrdiff_t)(n * z), v.data.begin() + (std::ptrdiff_t)(n * (z + 1)),
+            out.data.begin());
+  return out;
+}
+
+// Worker count (core.hpp:50-60).  The reference's OpenMP width has no GPU
+// meaning: every call runs on one device stream, results never depend on it.
+inline void set_worker_count(int) {}
+inline int worker_count() { return 1; }
+namespace detail {
+inline int effective_workers() { return 1; }
+}  // namespace detail
+
+// rsf::KernelProfile (rsf.hpp:64-69): the reference's 14 stage rows
+// (rsf.cpp:228-233).  Filled from per-kernel CUDA events; the kernels fuse
+// stages, so each kernel's time lands on one row and the rows fused into it
+// stay 0 (rsfg.h, RSFG_STAGE_COUNT; carrier(i) names the row).
+struct KernelProfile {
+  static constexpr int kCount = RSFG_STAGE_COUNT;
+  static const std::array<const char*, kCount>& names() {
+    static const std::array<const char*, kCount> n = [] {
+      std::array<const char*, kCount> a{};
+      for (int i = 0; i < kCount; ++i) a[i] = rsfg_stage_name(i);
+      return a;
+    }();
+    return n;
+  }
+  static int carrier(int i) { return rsfg_stage_carrier(i); }
+  std::array<double, kCount> seconds{};
+  long iterations = 0;
+};
+
+// rsf::EvolveWorkspace (rsf.hpp:72-77): the scratch fields live on the device
+// inside the EvolutionState; kept so evolve_step has the reference signature.
+struct EvolveWorkspace {};
+
+// rsf::evolve (rsf.hpp:97-98), same signature; `options` (appended) selects
+// the device and the convolution form (RSFG_FIELDS_2 default, RSFG_FIELDS_4
+// the reference form).
 inline Volume evolve(Volume phi0, const Volume& I, const RsfParams& p, StopCheck stop = nullptr,
-                     int stop_every = 25, const rsfg_options* options = nullptr) {
+                     int stop_every = 25, KernelProfile* profile = nullptr, const rsfg_options* options = nullptr) {
   p.validate();
   check_same_dims(phi0, I, "evolve");
   const rsfg_params cp = p.c();
+  rsfg_options o;
+  rsfg_options_default(&o);
+  if (options) o = *options;
+  o.profile_stages = profile ? 1 : 0;
   struct Ctx {
     StopCheck* stop;
   } ctx{&stop};
@@ -118,8 +177,13 @@ inline Volume evolve(Volume phi0, const Volume& I, const RsfParams& p, StopCheck
     std::memcpy(v.data.data(), phi, v.voxels() * sizeof(float));
     return (*c->stop)(v, it) ? 1 : 0;
   };
-  check(rsfg_evolve(I.data.data(), phi0.data.data(), I.dims.nx, I.dims.ny, I.dims.nz, &cp, options,
-                    stop ? +tramp : nullptr, &ctx, stop_every, nullptr));
+  rsfg_report rep{};
+  check(rsfg_evolve(I.data.data(), phi0.data.data(), I.dims.nx, I.dims.ny, I.dims.nz, &cp, &o,
+                    stop ? +tramp : nullptr, &ctx, stop_every, &rep));
+  if (profile) {
+    for (int k = 0; k < KernelProfile::kCount; ++k) profile->seconds[k] += rep.stage_seconds[k];
+    profile->iterations += rep.iterations;
+  }
   return phi0;
 }
 
@@ -131,7 +195,8 @@ inline Volume extract_mask(const Volume& phi, int device = 0) {
 }
 
 // rsf::EvolutionState + init_evolution / evolve_step / energy (rsf.hpp:54-88),
-// with the state resident on the GPU.
+// with the state resident on the GPU (phi, K1*I / K2*I, the kernels, the
+// image range).  phi() downloads the current level set.
 class EvolutionState {
  public:
   EvolutionState(const Volume& phi0, const Volume& I, const RsfParams& p,
@@ -156,32 +221,100 @@ class EvolutionState {
     check(rsfg_state_read_phi(s_, v.data.data()));
     return v;
   }
-  rsfg_state* handle() { return s_; }
+  const Dims& dims() const { return dims_; }
+  rsfg_state* handle() const { return s_; }
 
  private:
-  friend double evolve_step(EvolutionState&);
-  friend Volume energy(EvolutionState&);
+  // evolve_step takes p on every call (rsf.cpp:324-357): push changed scalars.
+  void sync_params(const RsfParams& p) {
+    if (p.epsilon == p_.epsilon && p.alpha == p_.alpha && p.beta == p_.beta && p.dt == p_.dt &&
+        p.denom_floor == p_.denom_floor && p.grad_floor == p_.grad_floor)
+      return;
+    const rsfg_params cp = p.c();
+    check(rsfg_state_set_params(s_, &cp));
+    const double s1 = p_.sigma1, s2 = p_.sigma2;
+    p_ = p;
+    p_.sigma1 = s1;
+    p_.sigma2 = s2;
+  }
+  friend double evolve_step(EvolutionState&, const Volume&, const RsfParams&, EvolveWorkspace&, KernelProfile*);
+  friend Volume energy(const EvolutionState&, const Volume&, const RsfParams&);
   rsfg_state* s_ = nullptr;
   Dims dims_;
   RsfParams p_;
 };
 
-inline EvolutionState init_evolution(const Volume& phi0, const Volume& I, const RsfParams& p,
+// rsf::init_evolution (rsf.hpp:79): phi0 by value, like the reference.
+inline EvolutionState init_evolution(Volume phi0, const Volume& I, const RsfParams& p,
                                      const rsfg_options* options = nullptr) {
   p.validate();
   return EvolutionState(phi0, I, p, options);
 }
 
-inline double evolve_step(EvolutionState& st) {
+// rsf::evolve_step (rsf.hpp:87-88), same signature.  I must be the image the
+// state was initialised with (its device copy is used); p's scalars apply to
+// this step, sigma stays the state's (st.k1/st.k2, rsf.cpp:299-300).
+inline double evolve_step(EvolutionState& st, const Volume& I, const RsfParams& p, EvolveWorkspace& ws,
+                          KernelProfile* profile = nullptr) {
+  (void)ws;
+  if (!(I.dims == st.dims_)) throw shape_error("evolve_step: image dims differ from the state's");
+  st.sync_params(p);
   double frac = 0.0;
-  check(rsfg_state_step(st.s_, &frac));
+  if (profile) {
+    double secs[RSFG_STAGE_COUNT] = {};
+    check(rsfg_state_step_profiled(st.s_, &frac, secs));
+    for (int k = 0; k < KernelProfile::kCount; ++k) profile->seconds[k] += secs[k];
+    profile->iterations += 1;  // rsf.cpp:355
+  } else {
+    check(rsfg_state_step(st.s_, &frac));
+  }
   return frac;
 }
 
-inline Volume energy(EvolutionState& st) {
+// rsf::energy (rsf.hpp:82): the update field E of the current state.
+inline Volume energy(const EvolutionState& st, const Volume& I, const RsfParams& p) {
+  p.validate();
+  if (!(I.dims == st.dims_)) throw shape_error("energy: image dims differ from the state's");
+  EvolutionState& m = const_cast<EvolutionState&>(st);  // logically const: phi is not advanced
+  m.sync_params(p);
   Volume E(st.dims_.nx, st.dims_.ny, st.dims_.nz);
   check(rsfg_state_energy(st.s_, E.data.data()));
   return E;
+}
+
+// Short forms (the state already holds I and p).
+inline double evolve_step(EvolutionState& st) {
+  double frac = 0.0;
+  check(rsfg_state_step(st.handle(), &frac));
+  return frac;
+}
+inline Volume energy(EvolutionState& st) {
+  Volume E(st.dims().nx, st.dims().ny, st.dims().nz);
+  check(rsfg_state_energy(st.handle(), E.data.data()));
+  return E;
+}
+
+// rsf::region_intensities (rsf.hpp:39-41) on the GPU.
+inline std::pair<Volume, Volume> region_intensities(const Volume& I, const Volume& phi, double sigma1,
+                                                    double epsilon, double denom_floor = 1e-8, int device = 0) {
+  check_same_dims(I, phi, "region_intensities");
+  Volume rp(I.dims.nx, I.dims.ny, I.dims.nz), rm(I.dims.nx, I.dims.ny, I.dims.nz);
+  check(rsfg_region_intensities(I.data.data(), phi.data.data(), I.dims.nx, I.dims.ny, I.dims.nz, sigma1, epsilon,
+                                denom_floor, rp.data.data(), rm.data.data(), device));
+  return {std::move(rp), std::move(rm)};
+}
+
+// rsf::directional_forces (rsf.hpp:47-50) on the GPU.
+inline std::pair<Volume, Volume> directional_forces(const Volume& I, const Volume& r_plus, const Volume& r_minus,
+                                                    const Volume& KI, const Volume& KI2, int device = 0) {
+  check_same_dims(I, r_plus, "directional_forces");
+  check_same_dims(I, r_minus, "directional_forces");
+  check_same_dims(I, KI, "directional_forces");
+  check_same_dims(I, KI2, "directional_forces");
+  Volume Fp(I.dims.nx, I.dims.ny, I.dims.nz), Fm(I.dims.nx, I.dims.ny, I.dims.nz);
+  check(rsfg_directional_forces(r_plus.data.data(), r_minus.data.data(), KI.data.data(), KI2.data.data(),
+                                (int64_t)I.voxels(), Fp.data.data(), Fm.data.data(), device));
+  return {std::move(Fp), std::move(Fm)};
 }
 
 // ---- seeding and curtain tiling around the hot path ------

@@ -297,4 +297,26 @@ int rsfref_read_volume(const char* header, float* out, long cap, int* nx, int* n
   })
 }
 
+// rsf::region_intensities (rsf.hpp:39-41, rsf.cpp:235-266).
+int rsfref_region_intensities(const float* I, const float* phi, int nx, int ny, int nz, double sigma1,
+                              double epsilon, double denom_floor, float* r_plus, float* r_minus) {
+  GUARD({
+    auto rr = rsf::region_intensities(make_vol(I, nx, ny, nz), make_vol(phi, nx, ny, nz), sigma1, epsilon,
+                                      denom_floor);
+    std::memcpy(r_plus, rr.first.data.data(), rr.first.voxels() * sizeof(float));
+    std::memcpy(r_minus, rr.second.data.data(), rr.second.voxels() * sizeof(float));
+  })
+}
+
+// rsf::directional_forces (rsf.hpp:47-50, rsf.cpp:268-291).
+int rsfref_directional_forces(const float* I, const float* rp, const float* rm, const float* KI, const float* KI2,
+                              int nx, int ny, int nz, float* Fp, float* Fm) {
+  GUARD({
+    auto ff = rsf::directional_forces(make_vol(I, nx, ny, nz), make_vol(rp, nx, ny, nz), make_vol(rm, nx, ny, nz),
+                                      make_vol(KI, nx, ny, nz), make_vol(KI2, nx, ny, nz));
+    std::memcpy(Fp, ff.first.data.data(), ff.first.voxels() * sizeof(float));
+    std::memcpy(Fm, ff.second.data.data(), ff.second.voxels() * sizeof(float));
+  })
+}
+
 }  // extern "C"

@@ -7,6 +7,8 @@ for tests and benchmarks; see api.py.
 from .api import (  # noqa: F401
     BlowupError,
     EvolutionState,
+    EvolveWorkspace,
+    KernelProfile,
     ParamError,
     RsfParams,
     ShapeError,
@@ -32,5 +34,7 @@ from .api import (  # noqa: F401
     phantom,
     phantom_device,
     threshold_phi0,
+    region_intensities,
+    directional_forces,
 )
 from ._lib import LIB_PATH, load  # noqa: F401

@@ -46,8 +46,12 @@ class rsfg_options(C.Structure):
         ("check_every", C.c_int32),
         ("use_graphs", C.c_int32),
         ("reuse_workspace", C.c_int32),
-        ("reserved", C.c_int32 * 3),
+        ("profile_stages", C.c_int32),
+        ("reserved", C.c_int32 * 2),
     ]
+
+
+RSFG_STAGE_COUNT = 14
 
 
 class rsfg_report(C.Structure):
@@ -63,6 +67,7 @@ class rsfg_report(C.Structure):
         ("ms_loop", C.c_double),
         ("ms_d2h", C.c_double),
         ("gpu_launches", C.c_int64),
+        ("stage_seconds", C.c_double * RSFG_STAGE_COUNT),
     ]
 
 
@@ -129,6 +134,15 @@ SIGNATURES = {
     "rsfg_state_energy": (C.c_int, [VP, FP]),
     "rsfg_state_profile": (C.c_int, [VP, I32, P(C.c_double)]),
     "rsfg_profile_name": (C.c_char_p, [I32]),
+    "rsfg_stage_name": (C.c_char_p, [I32]),
+    "rsfg_stage_carrier": (C.c_int32, [I32]),
+    "rsfg_state_step_profiled": (C.c_int, [VP, P(C.c_double), P(C.c_double)]),
+    "rsfg_state_set_params": (C.c_int, [VP, P(rsfg_params)]),
+    "rsfg_region_intensities": (C.c_int, [FP, FP, I32, I32, I32, C.c_double, C.c_double, C.c_double, FP, FP, I32]),
+    "rsfg_region_intensities_device": (C.c_int, [VP, VP, I32, I32, I32, C.c_double, C.c_double, C.c_double, VP,
+                                                 VP, I32]),
+    "rsfg_directional_forces": (C.c_int, [FP, FP, FP, FP, C.c_int64, FP, FP, I32]),
+    "rsfg_directional_forces_device": (C.c_int, [VP, VP, VP, VP, C.c_int64, VP, VP, I32]),
     "rsfg_state_read_phi": (C.c_int, [VP, FP]),
     "rsfg_state_write_phi": (C.c_int, [VP, FP]),
     "rsfg_state_mask": (C.c_int, [VP, FP]),

@@ -113,9 +113,39 @@ def gaussian_kernel(sigma: float) -> np.ndarray:
     return np.array(w[: 2 * r.value + 1])
 
 
-def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, *, fields: int = 2, device: int = 0,
-           report: L.rsfg_report | None = None) -> np.ndarray:
-    """rsf::evolve (rsf.cpp:359-384): returns the evolved phi (same shape as phi0)."""
+class KernelProfile:
+    """rsf::KernelProfile (rsf.hpp:64-69): the reference's 14 stage rows
+    (rsf.cpp:228-233) with seconds per row and the profiled iteration count.
+    The kernels fuse stages, so each kernel's CUDA-event time lands on one row
+    (``carrier``) and the rows fused into it stay 0 (include/rsfg.h,
+    RSFG_STAGE_COUNT)."""
+
+    kCount = L.RSFG_STAGE_COUNT
+
+    def __init__(self):
+        self.seconds = [0.0] * self.kCount
+        self.iterations = 0
+
+    @staticmethod
+    def names() -> list[str]:
+        lib = L.load()
+        return [lib.rsfg_stage_name(i).decode() for i in range(L.RSFG_STAGE_COUNT)]
+
+    @staticmethod
+    def carrier() -> list[int]:
+        lib = L.load()
+        return [int(lib.rsfg_stage_carrier(i)) for i in range(L.RSFG_STAGE_COUNT)]
+
+    def add(self, secs, iterations: int) -> None:
+        for i in range(self.kCount):
+            self.seconds[i] += float(secs[i])
+        self.iterations += iterations
+
+
+def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, profile: KernelProfile | None = None, *,
+           fields: int = 2, device: int = 0, report: L.rsfg_report | None = None) -> np.ndarray:
+    """rsf::evolve (rsf.cpp:359-384): returns the evolved phi (same shape as phi0).
+    ``profile`` (a KernelProfile) receives the per-row kernel seconds."""
     squeeze = np.ndim(phi0) == 2
     phi = _vol(phi0, "phi0").copy()
     img = _vol(I, "I")
@@ -123,6 +153,7 @@ def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, *, fields: in
     nz, ny, nx = phi.shape
     cp = p.to_c()
     opt = options(fields, device)
+    opt.profile_stages = 1 if profile is not None else 0
     rep = report if report is not None else L.rsfg_report()
     cb = L.STOP_FN(0)
     if stop is not None:
@@ -132,6 +163,8 @@ def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, *, fields: in
         cb = L.STOP_FN(_cb)
     check(L.load().rsfg_evolve(_ptr(img), _ptr(phi), nx, ny, nz, C.byref(cp), C.byref(opt), cb, None,
                                stop_every, C.byref(rep)))
+    if profile is not None:
+        profile.add(rep.stage_seconds, rep.iterations)
     return phi[0] if squeeze else phi
 
 
@@ -181,10 +214,21 @@ class EvolutionState:
         _check_same(a, np.empty(self.shape, np.float32), "phi")
         check(L.load().rsfg_state_write_phi(self._h, _ptr(a)))
 
-    def step(self) -> float:
+    def step(self, profile: KernelProfile | None = None) -> float:
         f = C.c_double()
-        check(L.load().rsfg_state_step(self._h, C.byref(f)))
+        if profile is None:
+            check(L.load().rsfg_state_step(self._h, C.byref(f)))
+        else:
+            secs = (C.c_double * L.RSFG_STAGE_COUNT)()
+            check(L.load().rsfg_state_step_profiled(self._h, C.byref(f), secs))
+            profile.add(secs, 1)
         return f.value
+
+    def set_params(self, p: RsfParams) -> None:
+        """Step scalars for the next steps (evolve_step takes p on every call);
+        sigma1/sigma2 stay the state's own."""
+        cp = p.to_c()
+        check(L.load().rsfg_state_set_params(self._h, C.byref(cp)))
 
     def run(self, n: int) -> L.rsfg_report:
         rep = L.rsfg_report()
@@ -242,14 +286,55 @@ def init_evolution(phi0, I, p: RsfParams, **kw) -> EvolutionState:
     return EvolutionState(phi0, I, p, **kw)
 
 
-def evolve_step(state: EvolutionState) -> float:
-    """rsf::evolve_step (rsf.cpp:324-357): returns the sign-change fraction."""
-    return state.step()
+class EvolveWorkspace:
+    """rsf::EvolveWorkspace (rsf.hpp:72-77): accepted for signature parity;
+    the device buffers live in the EvolutionState."""
 
 
-def energy(state: EvolutionState) -> np.ndarray:
-    """rsf::energy (rsf.cpp:315-322)."""
+def evolve_step(state: EvolutionState, I=None, p: RsfParams | None = None, ws: EvolveWorkspace | None = None,
+                profile: KernelProfile | None = None) -> float:
+    """rsf::evolve_step (rsf.hpp:87-88, rsf.cpp:324-357): returns the sign-change
+    fraction.  ``I`` must be the image the state was created with (its device
+    copy is used); ``p`` updates the step scalars (sigma stays the state's)."""
+    if I is not None:
+        _check_same(_vol(I, "I"), np.empty(state.shape, np.float32), "evolve_step")
+    if p is not None:
+        state.set_params(p)
+    return state.step(profile)
+
+
+def energy(state: EvolutionState, I=None, p: RsfParams | None = None) -> np.ndarray:
+    """rsf::energy (rsf.hpp:82, rsf.cpp:315-322)."""
+    if I is not None:
+        _check_same(_vol(I, "I"), np.empty(state.shape, np.float32), "energy")
+    if p is not None:
+        p.validate()
+        state.set_params(p)
     return state.energy()
+
+
+def region_intensities(I, phi, sigma1: float, epsilon: float, denom_floor: float = 1e-8, device: int = 0):
+    """rsf::region_intensities (rsf.hpp:39-41, rsf.cpp:235-266) on the GPU:
+    (r_plus, r_minus), the clamped local means on each side of the contour."""
+    img, ph = _vol(I, "I"), _vol(phi, "phi")
+    _check_same(img, ph, "region_intensities")
+    nz, ny, nx = img.shape
+    rp, rm = np.empty_like(img), np.empty_like(img)
+    check(L.load().rsfg_region_intensities(_ptr(img), _ptr(ph), nx, ny, nz, sigma1, epsilon, denom_floor, _ptr(rp),
+                                           _ptr(rm), device))
+    return rp, rm
+
+
+def directional_forces(I, r_plus, r_minus, KI, KI2, device: int = 0):
+    """rsf::directional_forces (rsf.hpp:47-50, rsf.cpp:268-291) on the GPU:
+    (F_plus, F_minus) = (KI2 - 2 r KI) + r^2 in f64."""
+    img = _vol(I, "I")
+    arrs = [_vol(a, n) for a, n in ((r_plus, "r_plus"), (r_minus, "r_minus"), (KI, "KI"), (KI2, "KI2"))]
+    for a in arrs:
+        _check_same(img, a, "directional_forces")
+    Fp, Fm = np.empty_like(img), np.empty_like(img)
+    check(L.load().rsfg_directional_forces(*(_ptr(a) for a in arrs), img.size, _ptr(Fp), _ptr(Fm), device))
+    return Fp, Fm
 
 
 def phantom(nx, ny, nz, n_branches=12, radius_min=2.0, radius_max=4.0, tortuosity=0.25, foreground=200.0,

@@ -88,10 +88,20 @@ int make_taps(double sigma, rsfg::Taps& t) {
 
 constexpr int kSlots = 64;  // per-iteration counter ring
 
+// Rows of the reference's 14-stage profile (rsf.cpp:46-61, names at
+// rsf.cpp:228-233) that carry a fused kernel's time: the Heaviside pass
+// when it runs as its own kernel; kernel 1 (Heaviside + y/x passes of the
+// (H, H I) pairs); kernel 2 (z pass, region means, forces, delta, gradient,
+// normalisation, curvature, Laplacian, combine, update).
+constexpr int kStageH = 0;        // "H-I"
+constexpr int kStageConv = 2;     // "K*H-I"
+constexpr int kStageCombine = 11; // "R-combine"
+
 }  // namespace
 
 namespace rsfg {
 void set_error(const std::string& msg) { g_err = msg; }
+int gaussian_taps(double sigma, Taps& t) { return make_taps(sigma, t); }
 }  // namespace rsfg
 
 // ------------------------------------------------------------------ engine
@@ -126,6 +136,13 @@ struct rsfg_slab {
   bool hh_mode = false;
   bool hh_valid = false;
   std::string env_key;  // kernel-variant environment at setup (workspace reuse must match it)
+  // Stage profiling (rsf::KernelProfile, rsf.hpp:64-69): while prof_on, every
+  // kernel launch of a step is bracketed by a CUDA-event pair tagged with the
+  // reference stage row that carries its time (kStage* below).
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;  // 2 per launch group
+  std::vector<int> prof_stage;
+  int prof_used = 0;
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -195,7 +212,48 @@ void release(rsfg_slab* s) {
   cudaFree(s->counters);
   cudaFree(s->mm);
   if (s->h_counters) cudaFreeHost(s->h_counters);
+  for (cudaEvent_t e : s->prof_ev) cudaEventDestroy(e);
+  s->prof_ev.clear();
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+int prof_begin(rsfg_slab* s) {
+  const int i = s->prof_used;
+  while ((int)s->prof_ev.size() < 2 * (i + 1)) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    s->prof_ev.push_back(e);
+  }
+  if ((int)s->prof_stage.size() < i + 1) s->prof_stage.resize(i + 1);
+  if (cudaEventRecord(s->prof_ev[2 * i], s->stream) != cudaSuccess) return -1;
+  s->prof_used = i + 1;
+  return i;
+}
+
+// Brackets the launches of one scope with an event pair (no-op unless prof_on).
+struct ProfScope {
+  rsfg_slab* s;
+  int stage, idx = -1;
+  ProfScope(rsfg_slab* s_, int st) : s(s_), stage(st) {
+    if (s->prof_on) idx = prof_begin(s);
+  }
+  ~ProfScope() {
+    if (idx < 0) return;
+    s->prof_stage[idx] = stage;
+    cudaEventRecord(s->prof_ev[2 * idx + 1], s->stream);
+  }
+};
+
+// Adds the recorded launch-group times to seconds[14] (syncs the stream).
+void prof_collect(rsfg_slab* s, double* seconds) {
+  if (s->prof_used == 0) return;
+  cudaStreamSynchronize(s->stream);
+  for (int i = 0; i < s->prof_used; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, s->prof_ev[2 * i], s->prof_ev[2 * i + 1]) == cudaSuccess && seconds)
+      seconds[s->prof_stage[i]] += 1e-3 * ms;
+  }
+  s->prof_used = 0;
 }
 
 void destroy_state(rsfg_state* st) {
@@ -412,6 +470,8 @@ int reconfigure(rsfg_slab* s, const rsfg_params* p, const rsfg_options* o) {
   s->valid = true;
   s->initialized = false;
   s->hh_valid = false;
+  s->prof_on = false;
+  s->prof_used = 0;
   return RSFG_OK;
 }
 
@@ -492,14 +552,17 @@ int xy_planes(rsfg_slab* s, int a, int b) {
   if (s->fast) {
     if (s->hh_mode && !(s->hh_valid && a >= s->z0 && b <= s->z1)) {
       // pairs of planes kernel 2 did not write for the current phi
+      ProfScope ps(s, kStageH);
       s->launches += rsfg::launch_hh(g, s->c.inv_eps, s->phi[s->cur], s->image, s->hh, a, b, s->stream);
     }
+    ProfScope ps(s, kStageConv);
     n = rsfg::launch_xy2(g, s->fields, s->xy2_ty, s->t1, s->c.inv_eps, s->P[0], s->P[1], a, b, s->xy2maps[s->cur],
                          s->stream);
     if (n < 0)
       n = rsfg::launch_xy(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P[0], s->P[1], a, b,
                           &s->xymaps[s->cur], s->stream);
   } else {
+    ProfScope ps(s, kStageConv);
     n = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
                                   s->scratch, a, b, 0, 0, s->stream);
   }
@@ -532,6 +595,7 @@ int step_finish(rsfg_slab* s, rsfg::StepMode mode, float* out) {
   rsfg::StepBuffers b = buffers(s, out);
   int n;
   if (s->fast) {
+    ProfScope ps(s, kStageCombine);
     n = -1;
     if (mode == rsfg::kUpdate) {
       b.hh = s->hh_mode ? s->hh : nullptr;
@@ -541,10 +605,15 @@ int step_finish(rsfg_slab* s, rsfg::StepMode mode, float* out) {
     }
     if (n < 0) n = rsfg::launch_zst(g, s->fields, s->t1, s->c, b, s->z0, s->z1, mode, s->stream);
   } else {
-    int m = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
-                                      s->scratch, 0, 0, s->z0, s->z1, s->stream);
+    int m;
+    {
+      ProfScope ps(s, kStageConv);
+      m = rsfg::launch_generic_conv(g, s->fields, s->t1, s->c.inv_eps, s->phi[s->cur], s->image, s->P,
+                                    s->scratch, 0, 0, s->z0, s->z1, s->stream);
+    }
     if (m < 0) return fail(RSFG_ERR_CUDA, "generic convolution launch failed");
     s->launches += m;
+    ProfScope ps(s, kStageCombine);
     n = rsfg::launch_zst(g, s->fields, s->tid, s->c, b, s->z0, s->z1, mode, s->stream);
   }
   if (n < 0) return fail(RSFG_ERR_CUDA, "step launch failed");
@@ -750,6 +819,63 @@ __attribute__((visibility("default"))) const char* rsfg_profile_name(int32_t i) 
   return (i >= 0 && i < 2) ? names[i] : "";
 }
 
+// The reference's 14 stage rows (rsf.cpp:228-233) and which row carries each
+// stage's time here (the kernels fuse them; kStage* above).
+namespace {
+const char* const kStageNames[RSFG_STAGE_COUNT] = {"H-I",  "H+I",      "K*H-I",     "K*H+I",       "K*H-",
+                                                   "K*H+", "delta",    "grad",      "grad-mag",    "laplacian",
+                                                   "grad/|grad|", "R-combine", "E+", "E-"};
+const int kStageCarrier[RSFG_STAGE_COUNT] = {kStageH,    kStageH,       kStageConv,    kStageConv,   kStageConv,
+                                             kStageConv, kStageCombine, kStageCombine, kStageCombine, kStageCombine,
+                                             kStageCombine, kStageCombine, kStageCombine, kStageCombine};
+}  // namespace
+
+__attribute__((visibility("default"))) const char* rsfg_stage_name(int32_t i) {
+  return (i >= 0 && i < RSFG_STAGE_COUNT) ? kStageNames[i] : "";
+}
+
+__attribute__((visibility("default"))) int32_t rsfg_stage_carrier(int32_t i) {
+  return (i >= 0 && i < RSFG_STAGE_COUNT) ? kStageCarrier[i] : -1;
+}
+
+__attribute__((visibility("default"))) int rsfg_state_step_profiled(rsfg_state* st, double* frac, double* seconds) {
+  if (!st || !seconds) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_slab* s = &st->e;
+  s->prof_used = 0;
+  s->prof_on = true;
+  int rc = rsfg_state_step(st, frac);
+  s->prof_on = false;
+  prof_collect(s, rc == RSFG_OK ? seconds : nullptr);
+  return rc;
+}
+
+// evolve_step(state, I, p, ...) takes p every call (rsf.cpp:324-357): the
+// scalar knobs (epsilon, alpha, beta, dt, floors) may change between steps;
+// the kernels (sigma1, sigma2) are the state's own (st.k1/st.k2, rsf.cpp:299-300).
+__attribute__((visibility("default"))) int rsfg_state_set_params(rsfg_state* st, const rsfg_params* p) {
+  if (!st) return fail(RSFG_ERR_STATE, "null state");
+  if (int rc = validate(p)) return rc;
+  rsfg_slab* s = &st->e;
+  const bool eps_changed = p->epsilon != s->p.epsilon;
+  const double sig1 = s->p.sigma1, sig2 = s->p.sigma2;
+  s->p = *p;
+  s->p.sigma1 = sig1;
+  s->p.sigma2 = sig2;
+  const double eps = p->epsilon;
+  s->c.inv_eps = (float)(1.0 / eps);
+  s->c.c_delta = (float)((1.0 / M_PI) * eps);
+  s->c.eps2 = (float)(eps * eps);
+  s->c.alpha = (float)p->alpha;
+  s->c.beta = (float)p->beta;
+  s->c.denom_floor = (float)p->denom_floor;
+  s->c.grad_floor = (float)p->grad_floor;
+  s->c.inv_grad_floor = (float)(1.0 / p->grad_floor);
+  s->c.dt = p->dt;
+  s->c.dt_f = (float)p->dt;
+  if (eps_changed) s->hh_valid = false;  // stored (H-, H- I) pairs used the old epsilon
+  return RSFG_OK;
+}
+
 __attribute__((visibility("default"))) int rsfg_state_energy(rsfg_state* st, float* E) {
   if (!st || !E) return fail(RSFG_ERR_STATE, "null argument");
   rsfg_slab* s = &st->e;
@@ -933,6 +1059,12 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
   cudaEventRecord(ev[2], s->stream);
 
   const bool per_step = p->convergence_fraction > 0.0;
+  s->prof_used = 0;
+  s->prof_on = opt.profile_stages != 0;  // KernelProfile* passed to evolve (rsf.cpp:359-384)
+  struct ProfOff {
+    rsfg_slab* s;
+    ~ProfOff() { s->prof_on = false; }
+  } prof_off{s};
   std::vector<float> host_phi;
   int pending = 0;
   const long long l0 = s->launches;
@@ -945,6 +1077,7 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
       long long sc = 0;
       int bad_it = 0;
       int rc = check_counters(s, pending, &sc, &bad_it);
+      prof_collect(s, rep->stage_seconds);
       pending = 0;
       rep->iterations = s->iteration;
       rep->last_sign_change_fraction = (double)sc / ((double)nx * ny * nz);

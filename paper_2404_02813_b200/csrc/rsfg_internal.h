@@ -138,6 +138,12 @@ int launch_hh(const Geom& g, float inv_eps, const float* phi, const float* image
 
 // Sets the calling thread's rsfg_last_error() message (rsfg_api.cu).
 void set_error(const std::string& msg);
+// gaussian_kernel (ops.cpp:9-29) as fp32 taps; RSFG_ERR_* with the message set.
+int gaussian_taps(double sigma, Taps& t);
+
+// Full 3-D separable convolution of a float2 pair field held in `a` (all
+// planes of g): x a->b, y b->a, z a->b; the result is left in b.
+int launch_conv_pair(const Geom& g, const Taps& t, float2* a, float2* b, cudaStream_t st);
 
 // phi0 initialisation (rsfg_seed.cu; reference seeding.cpp:83-235).
 struct SeedHost {

@@ -1,6 +1,7 @@
 // rsfg_kernels.cu -- support kernels: the generic-radius separable passes,
 // static-field convolutions (init), min/max, mask.  The two hot kernels are
-// in rsfg_xy.cu and rsfg_zst.cu.
+// xy2 (rsfg_xy2.cuh) and zst4 (rsfg_zst4.cuh); rsfg_xy.cu / rsfg_zst.cu hold
+// their LDG-staged fallbacks.
 #include <cstring>
 
 #include "rsfg_device.cuh"
@@ -147,6 +148,14 @@ int launch_convolve(const Geom& g, const Taps& t, const float* src, float* dst, 
   conv_axis_kernel<float><<<grid_for(n_xy, 256), 256, 0, st>>>(g, t, 0, src, tmp0, za, zb2);
   conv_axis_kernel<float><<<grid_for(n_xy, 256), 256, 0, st>>>(g, t, 1, tmp0, tmp1, za, zb2);
   conv_axis_kernel<float><<<grid_for(n_z, 256), 256, 0, st>>>(g, t, 2, tmp1, dst, z_begin, z_end);
+  return 3;
+}
+
+int launch_conv_pair(const Geom& g, const Taps& t, float2* a, float2* b, cudaStream_t st) {
+  const long long n = (long long)(g.ze - g.zb) * g.plane;
+  conv_axis_kernel<float2><<<grid_for(n, 256), 256, 0, st>>>(g, t, 0, a, b, g.zb, g.ze);
+  conv_axis_kernel<float2><<<grid_for(n, 256), 256, 0, st>>>(g, t, 1, b, a, g.zb, g.ze);
+  conv_axis_kernel<float2><<<grid_for(n, 256), 256, 0, st>>>(g, t, 2, a, b, g.zb, g.ze);
   return 3;
 }
 

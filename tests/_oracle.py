@@ -77,6 +77,9 @@ class Oracle:
                                     C.POINTER(Params), F32P]
         L.oracle_convolve.argtypes = [C.c_int, C.c_int, C.c_int, F32P, C.c_double, F32P]
         L.oracle_gaussian_kernel.argtypes = [C.c_double, np.ctypeslib.ndpointer(np.float64), C.c_int]
+        L.oracle_region_intensities.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, C.c_double, C.c_double,
+                                                C.c_double, F32P, F32P]
+        L.oracle_directional_forces.argtypes = [C.c_size_t, F32P, F32P, F32P, F32P, F32P, F32P]
 
     def gaussian_kernel(self, sigma):
         w = np.zeros(1024, np.float64)
@@ -121,6 +124,19 @@ class Oracle:
         out = np.empty_like(v)
         self.lib.oracle_convolve(nx, ny, nz, v, sigma, out)
         return out
+
+    def region_intensities(self, I, phi, sigma1, epsilon, denom_floor=1e-8):
+        """(r_plus, r_minus) -- rsf::region_intensities (rsf.cpp:235-266)."""
+        nx, ny, nz = _shape(I)
+        rp, rm = np.empty_like(I), np.empty_like(I)
+        self.lib.oracle_region_intensities(nx, ny, nz, I, phi, sigma1, epsilon, denom_floor, rp, rm)
+        return rp, rm
+
+    def directional_forces(self, r_plus, r_minus, KI, KI2):
+        """(F_plus, F_minus) -- rsf::directional_forces (rsf.cpp:268-291)."""
+        Fp, Fm = np.empty_like(KI), np.empty_like(KI)
+        self.lib.oracle_directional_forces(KI.size, r_plus, r_minus, KI, KI2, Fp, Fm)
+        return Fp, Fm
 
     def evolve(self, phi0, I, p: Params, iters=None):
         st = self.init(I, p)
@@ -187,6 +203,10 @@ class RefLib:
         L.rsfref_dice.argtypes = [F32P, F32P, C.c_int, C.c_int, C.c_int]
         L.rsfref_dice.restype = C.c_double
         L.rsfref_set_workers.argtypes = [C.c_int]
+        L.rsfref_region_intensities.argtypes = [F32P, F32P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                                C.c_double, F32P, F32P]
+        L.rsfref_directional_forces.argtypes = [F32P, F32P, F32P, F32P, F32P, C.c_int, C.c_int, C.c_int, F32P,
+                                                F32P]
         L.rsfref_workers.restype = C.c_int
 
     def _check(self, rc):
@@ -211,6 +231,18 @@ class RefLib:
         out = np.empty_like(v)
         self._check(self.lib.rsfref_convolve(v, nx, ny, nz, sigma, out))
         return out
+
+    def region_intensities(self, I, phi, sigma1, epsilon, denom_floor=1e-8):
+        nx, ny, nz = _shape(I)
+        rp, rm = np.empty_like(I), np.empty_like(I)
+        self._check(self.lib.rsfref_region_intensities(I, phi, nx, ny, nz, sigma1, epsilon, denom_floor, rp, rm))
+        return rp, rm
+
+    def directional_forces(self, I, r_plus, r_minus, KI, KI2):
+        nx, ny, nz = _shape(I)
+        Fp, Fm = np.empty_like(I), np.empty_like(I)
+        self._check(self.lib.rsfref_directional_forces(I, r_plus, r_minus, KI, KI2, nx, ny, nz, Fp, Fm))
+        return Fp, Fm
 
     def phantom(self, nx, ny, nz, n_branches=12, rmin=2.0, rmax=4.0, tortuosity=0.25, fg=200.0, bg=50.0,
                 seed=1, tree_connected=True, axial_blur=0.0, noise_sigma=20.0, contrast_axis=0, lo=1.0,

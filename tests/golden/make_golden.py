@@ -7,6 +7,10 @@ gaussian_kernel / generate_network / perturb / init_phi) via
 oracle/ref_shim.cpp.  Run here (where /root/reference exists):
 
     make -C oracle && python tests/golden/make_golden.py
+
+It also writes terms_golden.npz: rsf::region_intensities and
+rsf::directional_forces (rsf.cpp:235-291) on the same inputs
+(`python tests/golden/make_golden.py terms` writes only that file).
 """
 import sys
 from pathlib import Path
@@ -48,5 +52,24 @@ def main():
     print("wrote", HERE / "rsf_golden.npz", {k: v.shape for k, v in out.items()})
 
 
+def terms():
+    ref = RefLib()
+    ref.set_workers(1)
+    g = dict(np.load(HERE / "rsf_golden.npz"))
+    img, phi0 = g["img"], g["phi0"]
+    out = {}
+    for tag, s1 in {"s3": 3.0, "s15": 1.5}.items():
+        rp, rm = ref.region_intensities(img, phi0, s1, 1.0, 1e-8)
+        out[f"rplus_{tag}"], out[f"rminus_{tag}"] = rp, rm
+    st = ref.state(phi0, img, params(sigma1=3.0, sigma2=1.5))
+    KI, KI2, _, _ = st.static()
+    Fp, Fm = ref.directional_forces(img, out["rplus_s3"], out["rminus_s3"], KI, KI2)
+    out.update(KI_s2_15=KI, KI2_s2_15=KI2, Fplus=Fp, Fminus=Fm)
+    np.savez_compressed(HERE / "terms_golden.npz", **out)
+    print("wrote", HERE / "terms_golden.npz", sorted(out))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] != ["terms"]:
+        main()
+    terms()

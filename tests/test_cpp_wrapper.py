@@ -73,3 +73,50 @@ def test_cpp_wrapper_gpu_matches_api(wrapper_bin, tmp_path, ref):
     assert np.array_equal(load("pipe_mask.raw"), mask_p)
     assert np.array_equal(load("merged_from_dir.raw"), phi_p)  # spill_dir + load_manifest + merge_from_dir
     assert (tmp_path / "layout.manifest").exists() and len(list(tmp_path.glob("tile_z*.vmh"))) == 8
+
+
+PROFCHECK = ROOT / "oracle" / "_ref" / "profiling_check"
+STAGES = ["H-I", "H+I", "K*H-I", "K*H+I", "K*H-", "K*H+", "delta", "grad", "grad-mag", "laplacian",
+          "grad/|grad|", "R-combine", "E+", "E-"]  # rsf.cpp:228-233
+
+
+def _profcheck():
+    if Path("/root/reference/proj/src/profiling.cpp").exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "profcheck"], check=True, capture_output=True)
+    if not PROFCHECK.exists():
+        pytest.skip("oracle/_ref/profiling_check not built (reference sources absent)")
+    return PROFCHECK
+
+
+def _rows(text):
+    rows = {}
+    for line in text.splitlines()[2:]:
+        parts = line.split()
+        if parts and parts[0] != "total":
+            rows[" ".join(parts[:-2])] = (float(parts[-2]), float(parts[-1].rstrip("%")))
+    return rows
+
+
+def test_reference_profiling_cpp_compiles_against_wrapper():
+    """The reference's own src/profiling.cpp (profile_evolution /
+    profile_table, profiling.cpp:8-63) compiles UNMODIFIED against
+    include/rsfgpu.hpp (namespace swap -Drsf=rsfgpu) and links to librsfg.so;
+    its table lists the reference's 14 stage names in order."""
+    out = subprocess.run([str(_profcheck()), "table"], check=True, capture_output=True, text=True).stdout
+    assert list(_rows(out)) == STAGES
+
+
+@pytest.mark.gpu
+def test_reference_profile_evolution_on_gpu():
+    """profile_evolution (reference code) timing our kernels: the rows that
+    carry kernel time are non-zero, the stages fused into them read 0."""
+    import paper_2404_02813_b200 as rsf
+    out = subprocess.run([str(_profcheck()), "run", "64"], check=True, capture_output=True, text=True).stdout
+    rows = _rows(out)
+    assert list(rows) == STAGES
+    carrier = rsf.KernelProfile.carrier()
+    for i, name in enumerate(STAGES):
+        if carrier[i] != i:
+            assert rows[name][0] == 0.0, (name, rows[name])
+    assert rows["K*H-I"][0] > 0 and rows["R-combine"][0] > 0
+    assert abs(sum(v[1] for v in rows.values()) - 100.0) < 0.1

@@ -105,3 +105,31 @@ def test_slab_step_matches_monolithic(oracle):
                                    np.ascontiguousarray(st[0][zb:ze]), np.ascontiguousarray(st[1][zb:ze]),
                                    st[2], st[3], p, z0, z1)
     assert np.array_equal(out[z0 - zb:z1 - zb], ref[z0:z1])
+
+
+TERMS = Path(__file__).resolve().parent / "golden" / "terms_golden.npz"
+
+
+def test_oracle_term_apis_vs_golden(oracle, gold):
+    """region_intensities / directional_forces (rsf.cpp:235-291): restatement
+    against the reference-generated vectors."""
+    t = dict(np.load(TERMS))
+    img, phi0 = gold["img"], gold["phi0"]
+    for tag, s1 in {"s3": 3.0, "s15": 1.5}.items():
+        rp, rm = oracle.region_intensities(img, phi0, s1, 1.0)
+        assert _rel(rp, t[f"rplus_{tag}"]) <= 1e-6 and _rel(rm, t[f"rminus_{tag}"]) <= 1e-6
+    Fp, Fm = oracle.directional_forces(t["rplus_s3"], t["rminus_s3"], t["KI_s2_15"], t["KI2_s2_15"])
+    assert np.array_equal(Fp, t["Fplus"]) and np.array_equal(Fm, t["Fminus"])
+
+
+def test_oracle_term_apis_bitwise_vs_reference(oracle, ref):
+    from _inputs import random_case
+    img, phi = random_case(28, 22, 18, seed=11)
+    for s1, eps in [(2.0, 1.0), (3.0, 0.5)]:
+        a = oracle.region_intensities(img, phi, s1, eps)
+        b = ref.region_intensities(img, phi, s1, eps)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    KI, KI2, _, _ = oracle.init(img, params(sigma2=1.5))
+    a = oracle.directional_forces(b[0], b[1], KI, KI2)
+    c = ref.directional_forces(img, b[0], b[1], KI, KI2)
+    assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1])
