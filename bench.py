@@ -2,24 +2,43 @@
 """Benchmark: RSF level-set evolution, voxel-iterations/s (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode weak|strong-cfg4|strong-cfg5] [--transport ipc|nccl|host]
 
 A "step" is one RSF iteration (rsf::evolve_step, rsf.cpp:324-357) over the
-whole volume.  Workload (BASELINE.json configs[1], SURVEY.md 8(d) cfg 2):
-512^3 synthetic tube network (reference phantom spec, n_branches 192, noise
-sigma 20), sigma1 = 3 (R = 9), sigma2 = 0, 3d-paper parameters, phi0 =
-threshold initialisation.  N > 1 scales WEAKLY: each GPU owns a 512^3 z-slab
-of a 512x512x(512 N) volume, with per-step NCCL halo exchange
-(paper_2404_02813_b200/spmd.py).
+whole volume.
+
+N = 1 (default): BASELINE.json configs[1] = SURVEY.md 8(d) cfg 2 -- 512^3
+synthetic tube network (reference phantom spec, n_branches 192, noise sigma
+20), sigma1 = 3 (R = 9), sigma2 = 0, 3d-paper parameters, phi0 = threshold
+initialisation.
+
+N > 1: `--gpus N` launches N ranks itself (torch.distributed.run, one process
+per GPU, 127.0.0.1) unless it is already running under torchrun; it refuses
+to run with fewer than N visible GPUs (unless --share-gpu).  Modes:
+  weak         each rank owns a 512^3 z-slab of 512 x 512 x (512 N) at the
+               cfg-2 density (BASELINE metric "512^3 ... (1/2/4/8 B200)");
+  strong-cfg4  cfg 4: 1024^3 light-sheet-like volume split over N ranks;
+  strong-cfg5  cfg 5: 2048 x 2048 x 1024 micro-CT-like volume, sigma1 = 4.
+The halo data path is the peer-link exchange (`--transport ipc`: boundary
+planes pushed into the neighbours' halo rows over NVLink via CUDA IPC, flag
+words instead of messages); `nccl` (send/recv) and `host` (gloo, host-staged)
+are the alternatives.
 
 `value`   : device-resident inputs, CUDA events around exactly K steps on the
-            launching stream, max over ranks.  Inputs (1.5 GiB working set)
-            are larger than L2, so no flush is needed.
+            launching stream, max over ranks.  Inputs (>= 1.5 GiB working
+            set) are larger than L2, so no flush is needed.
 `e2e`     : the same metric through the public C-ABI with HOST buffers
-            (rsfg_evolve: H2D of I and phi0, init, the config's 200
-            iterations, D2H of phi), wall clock per call.
-`roofline`: dominant kernel, algorithmic bytes per launch / CUDA-event time.
+            (rsfg_evolve: H2D of I and phi0, init, the config's iterations,
+            D2H of phi) per call, wall clock.  The headline is PAGEABLE host
+            memory (a std::vector, as the reference's caller passes it,
+            tiling.cpp:251); pinned buffers are reported beside it.
+`roofline`: the dominant kernel; achieved = SURVEY.md 8(d)'s 12 B per
+            voxel-iteration x the voxels one launch processes / its average
+            CUDA-event launch time (its share of the step is in kernel_share).
 `cpu_baseline`: the reference compiled from its own sources (oracle/_ref,
-            all host cores) on a bounded z-slab sample of the same volume.
+            all host cores) on the same 512^3 volume.
+`parity`  : 1-step |dphi| vs the reference at 512^3, and cfg 1 (128^3 x 100
+            iterations) mask statistics vs the reference.
 `--impl reference`: the reference CPU implementation alone (rank 0).
 """
 from __future__ import annotations
@@ -27,7 +46,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -45,34 +66,56 @@ SIGMA1 = 3.0
 ITERS_CFG = 200  # configs[1]: 200 iterations
 PHANTOM = dict(n_branches=192, radius_min=2.0, radius_max=4.0, tortuosity=0.25, foreground=200.0,
                background=50.0, rng_seed=1, tree_connected=True, noise_sigma=20.0, noise_seed=7)
+# SURVEY.md 8(d) cfg 4 / cfg 5 (strong scaling); iterations 100 each.
+STRONG = {
+    "strong-cfg4": dict(shape=(1024, 1024, 1024), sigma1=3.0, iters=100,
+                        spec=dict(n_branches=768, axial_blur_sigma=2.0, noise_sigma=25.0, contrast_axis=3,
+                                  contrast_lo=0.6, contrast_hi=1.0),
+                        workload="cfg4: 1024^3 light-sheet-like tube network (768 branches, axial blur 2, "
+                                 "z contrast 0.6-1.0, noise 25), sigma1=3 (R=9)"),
+    "strong-cfg5": dict(shape=(2048, 2048, 1024), sigma1=4.0, iters=100,
+                        spec=dict(n_branches=3072, radius_max=5.0, noise_sigma=15.0),
+                        workload="cfg5: 2048x2048x1024 micro-CT-like tube network (3072 branches, r 2-5, "
+                                 "noise 15), sigma1=4 (R=12)"),
+}
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
-# Implementation bytes per voxel each kernel must move at minimum.
-KERNEL_BYTES = {2: {"xy": 16, "zst": 24}, 4: {"xy": 24, "zst": 32}}
-ALGO_BYTES_STEP = 12  # read phi, read I, write phi' (fp32, sigma2 = 0)
+ALGO_BYTES = 12  # read phi, read I, write phi' (fp32, sigma2 = 0) per voxel-iteration
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d, "measured"
-    return PEAKS_FALLBACK, "fallback"
+        if "hbm_gbs" in d:
+            return {"hbm_gbs": float(d["hbm_gbs"])}, "measured (hbm_gbs, MEASURED_PEAKS.json)"
+        return PEAKS_FALLBACK, "fallback (MEASURED_PEAKS.json has no HBM key)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
-def workload_config(n_gpus, fields):
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_config(n_gpus, fields, mode="weak"):
     return {"workload": "cfg2: 512^3 synthetic tube network (SURVEY.md 8(d)), sigma1=3 (R=9), sigma2=0, "
                         "3d-paper params (alpha=58.5225, beta=0.1, eps=1, dt=0.06), phi0 = threshold init",
             "nx": NX, "ny": NY, "nz": NZ, "sigma1": SIGMA1, "sigma2": 0.0, "fields": fields,
-            "iterations_per_job": ITERS_CFG,
+            "iterations_per_job": ITERS_CFG, "mode": mode,
             "decomposition": f"z-slabs x{n_gpus}" if n_gpus > 1 else "single volume",
             "l2": "inputs larger than L2 (1.5 GiB working set vs 126 MB L2); no flush"}
 
 
 def make_inputs():
     import paper_2404_02813_b200 as rsf
-    img, _gt = rsf.phantom(NX, NY, NZ, **PHANTOM)
+    img, gt = rsf.phantom(NX, NY, NZ, **PHANTOM)
     phi0 = rsf.threshold_phi0(img)
-    return img, phi0
+    return img, phi0, gt
 
 
 class ClockSampler:
@@ -81,7 +124,7 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
 
-    def __init__(self, index=0, period=0.01):
+    def __init__(self, index=0, period=0.005):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
         self.period = period
@@ -122,15 +165,15 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def ncu_traffic(kernel_key):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(kernel_key, config):
+    """dram bytes per launch of that kernel from the committed ncu --set full summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
         k = d.get("kernels", {}).get(kernel_key)
-        if k and k.get("config") == f"{NX}x{NY}x{NZ}":
+        if k and k.get("config") == config:
             return k.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -144,40 +187,57 @@ def reference_lib():
     return RefLib()
 
 
-def reference_sample(img, phi0, planes):
-    """A z-slab sample [0, planes) of the same volume (reference is per-voxel rate
-    limited once data exceed L3)."""
-    return np.ascontiguousarray(img[:planes]), np.ascontiguousarray(phi0[:planes])
-
-
-def run_reference(img, phi0, steps, warmup, planes):
+def run_reference(img, phi0, steps, warmup, planes=None):
+    """Reference init_evolution + `warmup` untimed + `steps` timed evolve_step
+    (all host cores) on planes [0, planes) (default: the whole volume).
+    Returns (rate, cores, voxels, times, phi after the first step)."""
     ref = reference_lib()
     from _oracle import params as ref_params
     ref.set_workers(0)  # all host cores (volume.cpp:18-22)
-    si, sp = reference_sample(img, phi0, planes)
-    st = ref.state(sp, si, ref_params(sigma1=SIGMA1, sigma2=0.0))
-    for _ in range(warmup):
+    if planes is not None and planes < img.shape[0]:
+        img, phi0 = np.ascontiguousarray(img[:planes]), np.ascontiguousarray(phi0[:planes])
+    st = ref.state(phi0, img, ref_params(sigma1=SIGMA1, sigma2=0.0))
+    phi1 = None
+    for i in range(warmup):
         st.step()
+        if i == 0:
+            phi1 = st.phi()
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         st.step()
         times.append(time.perf_counter() - t0)
-    vox = si.size
-    rate = vox * steps / sum(times)
-    return rate, ref.workers(), vox, times
+    return img.size * steps / sum(times), ref.workers(), img.size, times, phi1
+
+
+def parity_cfg1(lib_ref):
+    """cfg 1: 128^3, 12 branches, noise 20, phi0 = the
+    reference's init_phi; 100 iterations on the GPU and in the reference.
+    BASELINE.md 3 statistics: mask sign-mismatch, Dice(GPU, CPU), Dice vs gt."""
+    import paper_2404_02813_b200 as rsf
+    from _oracle import params as ref_params
+    img, gt = lib_ref.phantom(128, 128, 128, n_branches=12, seed=1, noise_sigma=20.0, noise_seed=7)
+    phi0, _ = lib_ref.init_phi(img)
+    want = lib_ref.evolve(phi0, img, ref_params(sigma1=3.0, max_iters=100))
+    got = rsf.evolve(phi0, img, rsf.RsfParams(sigma1=3.0, max_iters=100))
+    mg, mr, mt = got < 0, want < 0, gt > 0.5
+    mism = int(np.count_nonzero(mg != mr))
+    return {"config": "cfg1: 128^3, 12 branches, noise 20, phi0 = reference init_phi, sigma1=3, 100 iterations",
+            "mask_mismatch": mism, "mask_mismatch_frac": mism / img.size,
+            "dice_gpu_vs_ref": rsf.dice(mg, mr), "dice_gt_gpu": rsf.dice(mg, mt), "dice_gt_ref": rsf.dice(mr, mt),
+            "gates": "P3: mismatch <= 1e-5 N, Dice(gpu, ref) >= 0.9999 (SURVEY.md 8(c))"}
 
 
 # ---------------------------------------------------------------------- GPU
 def bench_single(args):
+    import ctypes as C
     import torch
     import paper_2404_02813_b200 as rsf
     from paper_2404_02813_b200 import _lib as L
     from paper_2404_02813_b200.api import check, options
-    import ctypes as C
 
     torch.cuda.set_device(0)
-    img, phi0 = make_inputs()
+    img, phi0, gt = make_inputs()
     nvox = img.size
     p = rsf.RsfParams(sigma1=SIGMA1, sigma2=0.0, max_iters=ITERS_CFG)
     lib = rsf.load()
@@ -198,7 +258,7 @@ def bench_single(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = lib.rsfg_state_launches(h)
-    remaining, chunks = args.steps, []
+    remaining = args.steps
     with ClockSampler() as clk:
         torch.cuda.synchronize()
         e0.record(stream)
@@ -213,7 +273,7 @@ def bench_single(args):
     ms_step = ms / args.steps
     value = nvox * args.steps / (ms / 1e3)
 
-    # ---- per-kernel CUDA-event profile (same stream the kernels launch on)
+    # ---- per-kernel CUDA-event profile on the kernels' own stream
     prof = (C.c_double * 2)()
     check(lib.rsfg_state_profile(h, 10, prof))
     kern = {"xy": prof[0], "zst": prof[1]}
@@ -223,53 +283,84 @@ def bench_single(args):
     del d_img, d_phi
     torch.cuda.empty_cache()
 
-    pk, pk_kind = peaks()
+    pk, pk_src = peaks()
     peak = pk["hbm_gbs"]
     dom = max(kern, key=kern.get)
-    kb = dict(KERNEL_BYTES[args.fields])
-    kb.update(xy=xyb.value, zst=zstb.value)
-    achieved = kb[dom] * nvox / (kern[dom] * 1e-3) / 1e9
-    traffic = ncu_traffic(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_voxel": kb[dom], "peak_source": f"{pk_kind} hbm_gbs",
-                "kernel_variant_flags": vflags.value,
-                "bytes_note": "per-kernel minimum HBM bytes per voxel (rsfg_state_variant): kernel 2 also "
-                              "writes the (H-, H- I) pairs in the stored-Heaviside mode (flag 4)",
+    achieved = ALGO_BYTES * nvox / (kern[dom] * 1e-3) / 1e9
+    own = {"xy": xyb.value, "zst": zstb.value}
+    roofline = {"bound": "hbm", "kernel": {"xy": "kernel 1 (xy2_hh)", "zst": "kernel 2 (zst4)"}[dom],
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": ncu_traffic(dom, f"{NX}x{NY}x{NZ}"),
+                "algorithmic_bytes_per_voxel": ALGO_BYTES, "launch_ms": round(kern[dom], 4),
+                "peak_source": pk_src, "kernel_variant_flags": vflags.value,
+                "basis": "SURVEY.md 8(d): 12 B per voxel-iteration x 512^3 voxels per launch / the launch's "
+                         "CUDA-event time",
+                "kernel_own_min_bytes_per_voxel": own,
+                "kernel_own_frac": {k: round(own[k] * nvox / (kern[k] * 1e-3) / 1e9 / peak, 4) for k in kern},
                 "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
-                "kernel_share": {k: round(v / sum(kern.values()), 3) for k, v in kern.items()}}
-    step_gbs = ALGO_BYTES_STEP * value / 1e9
-    step_roofline = {"bytes_per_voxel_iter": ALGO_BYTES_STEP, "achieved": round(step_gbs, 1),
-                     "frac": round(step_gbs / peak, 4), "unit": "GB/s",
-                     "note": "fused-minimum 12 B/voxel-iter (SURVEY.md 8(d)) over the whole step"}
+                "kernel_share": {k: round(v / sum(kern.values()), 3) for k, v in kern.items()},
+                "step_frac": round(ALGO_BYTES * value / 1e9 / peak, 4)}
 
-    # ---- e2e: public C-ABI with pinned host buffers, H2D + D2H inside the timed region
-    h_img = torch.from_numpy(img).pin_memory()
-    h_phi = torch.empty_like(h_img).pin_memory()
-    e2e_times, rep2 = [], L.rsfg_report()
-    opt2 = options(args.fields, 0, 25)
-    for i in range(1 + args.e2e_steps):
-        h_phi.copy_(torch.from_numpy(phi0))
-        t0 = time.perf_counter()
-        check(lib.rsfg_evolve(h_img.data_ptr(), h_phi.data_ptr(), NX, NY, NZ, C.byref(cp), C.byref(opt2),
-                              L.STOP_FN(0), None, 0, C.byref(rep2)))
-        dt = time.perf_counter() - t0
-        if i > 0:
-            e2e_times.append(dt)
-    e2e_value = nvox * ITERS_CFG / statistics.median(e2e_times) if e2e_times else None
-    e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
-           "iterations_per_step": ITERS_CFG, "api": "rsfg_evolve (host buffers)",
-           "phase_ms": {"h2d": round(rep2.ms_h2d, 2), "init": round(rep2.ms_init, 2),
-                        "loop": round(rep2.ms_loop, 2), "d2h": round(rep2.ms_d2h, 2)}}
+    # ---- 14-row stage profile (rsf::KernelProfile) over a few steps
+    stage = rsf.KernelProfile()
+    st = rsf.init_evolution(phi0, img, p, fields=args.fields)
+    for _ in range(3):
+        st.step(stage)
+    stage_rows = {n: round(1e3 * s / max(1, stage.iterations), 4)
+                  for n, s in zip(rsf.KernelProfile.names(), stage.seconds)}
+    st.close()
 
-    # ---- CPU baseline: the reference itself on a bounded sample of the same volume
-    cpu = None
+    # ---- e2e: public C-ABI with HOST buffers, H2D + D2H inside the timed region
+    def e2e_run(phi_buf, img_buf):
+        times, rep2 = [], L.rsfg_report()
+        opt2 = options(args.fields, 0, 25)
+        for i in range(1 + args.e2e_steps):
+            np.copyto(phi_buf, phi0)
+            t0 = time.perf_counter()
+            check(lib.rsfg_evolve(img_buf.ctypes.data, phi_buf.ctypes.data, NX, NY, NZ, C.byref(cp), C.byref(opt2),
+                                  L.STOP_FN(0), None, 0, C.byref(rep2)))
+            dt = time.perf_counter() - t0
+            if i > 0:
+                times.append(dt)
+        return nvox * ITERS_CFG / statistics.median(times), rep2
+
+    page_img, page_phi = np.array(img), np.empty_like(phi0)  # ordinary (pageable) host memory
+    e2e_page, rep_page = e2e_run(page_phi, page_img)
+    phi_gpu_final = page_phi.copy()
+    t_img = torch.from_numpy(img).pin_memory()
+    t_phi = torch.empty_like(t_img).pin_memory()
+    e2e_pin, rep_pin = e2e_run(t_phi.numpy(), t_img.numpy())
+    del t_img, t_phi
+
+    def phases(r):
+        return {"h2d": round(r.ms_h2d, 2), "init": round(r.ms_init, 2), "loop": round(r.ms_loop, 2),
+                "d2h": round(r.ms_d2h, 2)}
+
+    e2e = {"value": e2e_page, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
+           "iterations_per_step": ITERS_CFG, "host_memory": "pageable (numpy / std::vector, as tiling.cpp:251)",
+           "api": "rsfg_evolve (host buffers; device workspace allocated and freed inside every call)",
+           "phase_ms": phases(rep_page),
+           "pinned": {"value": e2e_pin, "phase_ms": phases(rep_pin)}}
+
+    # ---- CPU baseline + parity: the reference itself on the same 512^3 volume
+    cpu, parity = None, None
     if not args.no_cpu:
         try:
-            rate, cores, vox, times = run_reference(img, phi0, steps=3, warmup=1, planes=args.cpu_planes)
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"reference init_evolution + 1 warm-up + 3 timed evolve_step on planes "
-                             f"[0,{args.cpu_planes}) of the same 512^3 volume ({vox} voxels)"}
+            rate, cores, vox, times, ref_phi1 = run_reference(img, phi0, steps=2, warmup=1)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
+                   "sample": f"reference init_evolution + 1 warm-up + 2 timed evolve_step on the full 512^3 "
+                             f"volume ({vox} voxels), all {cores} host threads"}
+            st1 = rsf.init_evolution(phi0, img, p, fields=args.fields)
+            st1.step()
+            g1 = st1.phi
+            st1.close()
+            d = np.abs(g1.astype(np.float64) - ref_phi1)
+            parity = {"cfg2_step1": {"max_abs_dphi": float(d.max()),
+                                     "max_rel_dphi": float((d / np.maximum(1.0, np.abs(ref_phi1))).max()),
+                                     "gate": "P1 max|dphi| <= 1e-4 (SURVEY.md 8(c))"},
+                      "cfg2_200it_gpu_dice_vs_gt": rsf.dice(phi_gpu_final < 0, gt > 0.5)}
+            if not args.no_parity:
+                parity["cfg1_100it"] = parity_cfg1(reference_lib())
         except Exception as e:  # reference build missing on this host
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -277,60 +368,76 @@ def bench_single(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference phantom spec, seeded)",
-           "config": workload_config(1, args.fields), "roofline": roofline, "step_roofline": step_roofline,
-           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
-    print(json.dumps(out))
+           "config": workload_config(1, args.fields), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "parity": parity, "stage_ms_per_iter": stage_rows, "gpu_launches": launches, "clocks": clk.summary()}
+    print(json.dumps(out), flush=True)
 
 
-def bench_multi(args):
-    """N > 1: weak scaling.  The volume is 512 x 512 x (512 N) (the cfg-2 tube
-    network with 192 N branches, same density), one 512^3 z-slab per rank
-    (SURVEY.md 8(e)): per-step NCCL halo exchange of R planes each way,
-    overlapped with the owned planes' xy work.  Every rank generates the same
-    volume on its own GPU (device phantom, bit-exact with the reference
-    generator) and uploads only its held planes.  value = all voxels x K steps
-    / max over ranks of the CUDA-event time.  --backend gloo --share-gpu runs
-    the same path with ranks sharing cuda:0 and host-staged halos (1-GPU test
-    boxes)."""
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def bench_multi(args, world, rank, local):
+    """Multi-rank modes (module docstring).  value = all voxels x K steps /
+    max over ranks of the CUDA-event time of the K steps."""
     import torch
     import torch.distributed as dist
     import paper_2404_02813_b200 as rsf
-    from paper_2404_02813_b200.spmd import DistSlab, Slab
+    from paper_2404_02813_b200.spmd import DistSlab
 
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    if args.backend == "nccl":
+    if world == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    elif args.transport in ("nccl", "ipc") and not args.share_gpu:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         dist.init_process_group("gloo")
-    transport = "device" if args.backend == "nccl" else "host"
-    nz_total = NZ * world
-    spec = dict(PHANTOM)
-    spec["n_branches"] = PHANTOM["n_branches"] * world
-    img, _ = rsf.phantom_device(NX, NY, nz_total, with_gt=False, device=local,
+    transport = {"nccl": "device", "ipc": "ipc", "host": "host"}[args.transport]
+    if args.mode == "weak":
+        nx, ny, nz_total = NX, NY, NZ * world
+        spec = dict(PHANTOM)
+        spec["n_branches"] = PHANTOM["n_branches"] * world
+        sigma1, iters = SIGMA1, ITERS_CFG
+        workload = (f"weak scaling: 512x512x{nz_total} tube network (cfg2 density, {spec['n_branches']} branches), "
+                    "one 512^3 z-slab per GPU, sigma1=3 (R=9), 3d-paper params, phi0 = threshold init")
+        scaling = "weak"
+    else:
+        c = STRONG[args.mode]
+        nx, ny, nz_total = c["shape"]
+        spec = dict(PHANTOM)
+        spec.update(c["spec"])
+        sigma1, iters = c["sigma1"], c["iters"]
+        workload = c["workload"] + f", split into {world} z-slab(s), 3d-paper params, phi0 = threshold init"
+        scaling = "strong"
+    img, _ = rsf.phantom_device(nx, ny, nz_total, with_gt=False, device=local,
                                 **{k: v for k, v in spec.items() if k not in ("rng_seed", "noise_seed")},
                                 rng_seed=spec["rng_seed"], noise_seed=spec["noise_seed"])
     phi0 = torch.where(img > 125.0, -2.0, 2.0).to(torch.float32)
-    nvox = NX * NY * nz_total
-    p = rsf.RsfParams(sigma1=SIGMA1, sigma2=0.0, max_iters=ITERS_CFG)
+    nvox = nx * ny * nz_total
+    p = rsf.RsfParams(sigma1=sigma1, sigma2=0.0, max_iters=iters)
     ds = DistSlab(phi0, img, p, fields=args.fields, transport=transport)
-    # host copies of this rank's held planes for the e2e leg (outside any timing)
     zb, ze = ds.slab.zb, ds.slab.ze
-    h_img = torch.empty((nz_total, NY, NX), dtype=torch.float32).numpy()  # untouched planes stay unbacked
-    h_phi = torch.empty((nz_total, NY, NX), dtype=torch.float32).numpy()
-    h_img[zb:ze] = img[zb:ze].cpu().numpy()
-    h_phi[zb:ze] = phi0[zb:ze].cpu().numpy()
+    keep_host = args.e2e_steps > 0
+    if keep_host:  # host copies of this rank's held planes for the e2e leg (outside any timing)
+        h_img = np.zeros((nz_total, ny, nx), np.float32)  # untouched planes stay unbacked
+        h_phi = np.zeros((nz_total, ny, nx), np.float32)
+        h_img[zb:ze] = img[zb:ze].cpu().numpy()
+        h_phi[zb:ze] = phi0[zb:ze].cpu().numpy()
     del img, phi0
     torch.cuda.empty_cache()
+    red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     for _ in range(args.warmup):
         ds.step()
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ds.slab.launches()
-    red_dev = "cuda" if args.backend == "nccl" else "cpu"
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         dist.barrier()
@@ -348,14 +455,14 @@ def bench_multi(args):
     value = nvox * args.steps / (ms / 1e3)
     ds.slab.close()
 
-    # e2e: this rank's host planes -> device (H2D), init, ITERS_CFG steps, D2H of
-    # the owned planes; wall clock, max over ranks.
+    # e2e: this rank's host planes -> device, init, the config's iterations,
+    # D2H of the owned planes; wall clock, max over ranks.
     e2e_t = []
-    for i in range(1 + args.e2e_steps):
+    for i in range(1 + args.e2e_steps if keep_host else 0):
         dist.barrier()
         t0 = time.perf_counter()
         d2 = DistSlab(h_phi, h_img, p, fields=args.fields, transport=transport)
-        for _ in range(ITERS_CFG):
+        for _ in range(iters):
             d2.step()
         _ = d2.phi_owned()
         d2.slab.close()
@@ -364,23 +471,20 @@ def bench_multi(args):
         if i > 0:
             e2e_t.append(float(t.item()))
     if rank == 0:
-        cfg = workload_config(world, args.fields)
-        cfg.update({"workload": f"weak scaling: 512x512x{nz_total} tube network (cfg2 density, "
-                                f"{spec['n_branches']} branches), one 512^3 z-slab per GPU, sigma1=3 (R=9), "
-                                "3d-paper params, phi0 = threshold init",
-                    "nz": nz_total, "decomposition": f"z-slabs x{world}, halo R=9 planes each way per step "
-                                                     f"({args.backend}, overlapped with the owned planes' xy work)",
-                    "l2": "inputs larger than L2; no flush"})
+        cfg = {"workload": workload, "nx": nx, "ny": ny, "nz": nz_total, "sigma1": sigma1, "sigma2": 0.0,
+               "fields": args.fields, "iterations_per_job": iters, "mode": args.mode,
+               "decomposition": f"z-slabs x{world}, halo R planes each way per step ({args.transport})",
+               "transport": args.transport, "l2": "inputs larger than L2; no flush"}
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "scaling": scaling, "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (reference phantom spec, seeded; device generator)", "config": cfg,
-               "e2e": {"value": nvox * ITERS_CFG / statistics.median(e2e_t) if e2e_t else None, "unit": UNIT,
+               "e2e": {"value": nvox * iters / statistics.median(e2e_t) if e2e_t else None, "unit": UNIT,
                        "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
-                       "iterations_per_step": ITERS_CFG, "api": "spmd.DistSlab (host buffers)"},
+                       "iterations_per_step": iters, "api": "spmd.DistSlab (host buffers)"},
                "gpu_launches": int(launches.item()), "clocks": clk.summary(), "roofline": None,
                "cpu_baseline": None}
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     dist.destroy_process_group()
 
 
@@ -394,38 +498,67 @@ def bench_reference(args):
     img, _gt = ref.phantom(NX, NY, NZ, n_branches=PHANTOM["n_branches"], seed=PHANTOM["rng_seed"],
                            noise_sigma=PHANTOM["noise_sigma"], noise_seed=PHANTOM["noise_seed"])
     phi0 = np.where(img > 125, np.float32(-2.0), np.float32(2.0)).astype(np.float32)
-    budget_s = 120.0
-    planes = int(np.clip(3.0e7 * budget_s / max(1, args.steps + args.warmup) / (NX * NY), 16, 128))
-    rate, cores, vox, times = run_reference(img, phi0, steps=args.steps, warmup=args.warmup, planes=planes)
-    sample = f"{args.steps} timed evolve_step (after {args.warmup} warm-up) on planes [0,{planes}) of the 512^3 volume"
+    # The full 512^3 volume (about 2.5 s per step on 16 host cores) unless
+    # that would exceed ~5 minutes; then a z-slab sample, stated in `sample`.
+    planes = NZ
+    est_s = 2.6 * (args.steps + args.warmup)
+    if est_s > 300:
+        planes = int(np.clip(NZ * 300 / est_s, 16, NZ))
+    rate, cores, vox, times, _ = run_reference(img, phi0, steps=args.steps, warmup=args.warmup, planes=planes)
+    what = "the full 512^3 volume" if planes == NZ else f"planes [0,{planes}) of the 512^3 volume"
+    sample = (f"{args.steps} timed evolve_step (after init_evolution and {args.warmup} warm-up) on {what} "
+              f"({vox} voxels), {cores} host threads, {cpu_model()}")
     out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (reference)",
            "data": "synthetic (reference phantom spec, seeded)", "config": workload_config(1, 4),
            "impl": "reference",
-           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+                            "cpu_model": cpu_model()},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="weak", choices=["weak", *STRONG])
     ap.add_argument("--fields", type=int, default=2, choices=[2, 4])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-planes", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="N > 1 halo transport")
-    ap.add_argument("--share-gpu", action="store_true", help="N > 1 ranks all on cuda:0 (testing; gloo)")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl", "host"], help="N > 1 halo transport")
+    ap.add_argument("--backend", default=None, choices=["nccl", "gloo"], help="(legacy) gloo == --transport host")
+    ap.add_argument("--share-gpu", action="store_true", help="N > 1 ranks all on cuda:0 (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.backend == "gloo":
+        args.transport = "host" if args.transport == "nccl" else args.transport
+        args.share_gpu = True if args.transport == "host" else args.share_gpu
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    gpus = args.gpus if args.gpus is not None else world_env
+    if world_env > 1 and gpus != world_env:
+        sys.exit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world_env}")
+    if gpus > 1 and world_env == 1:
+        # one process per GPU: launch the N ranks ourselves
+        if not args.share_gpu and args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < gpus:
+                sys.exit(f"bench.py: --gpus {gpus} needs {gpus} visible GPUs, found {have}")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         return bench_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        return bench_multi(args)
+    rank = int(os.environ.get("RANK", "0"))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", rank))
+    if gpus > 1 or args.mode != "weak":
+        return bench_multi(args, gpus, rank, local)
     return bench_single(args)
 
 

@@ -235,6 +235,31 @@ int rsfg_slab_step_interior(rsfg_slab* s); /* work that needs no halo */
 int rsfg_slab_step_finish(rsfg_slab* s);   /* the rest; swaps phi      */
 /* Sign changes / first non-finite global index (-1) of the last step (syncs). */
 int rsfg_slab_counters(rsfg_slab* s, int64_t* sign_changes, int64_t* first_bad);
+
+/* Peer halo links: the B200-native exchange (no NCCL on the data path).  A
+ * linked slab, after each step, copies its new boundary phi planes straight
+ * into the neighbour's halo rows (NVLink peer memory; the same device works
+ * too) on a side stream and then stores the step number into the
+ * neighbour's flag word; the neighbour's stream waits for that flag
+ * (cuStreamWaitValue32) before its halo-dependent work, so the copy overlaps
+ * the next step's interior kernel-1 work.  One descriptor per slab, exchanged
+ * once: ipc = 0 for slabs in this process (raw pointers; peer access is
+ * enabled), ipc = 1 for another process on the node (CUDA IPC handles).
+ * Link side 0 to the slab below, side 1 to the slab above, then drive every
+ * slab with rsfg_slab_step_linked in lockstep (bitwise equal to one volume). */
+#define RSFG_PEER_DESC_BYTES 512
+int rsfg_slab_peer_desc(rsfg_slab* s, void* desc, int32_t ipc);
+int rsfg_slab_link(rsfg_slab* s, int32_t side, const void* peer_desc);
+int rsfg_slab_step_linked(rsfg_slab* s);
+
+/* rsf::evolve over n_devices GPUs of this process (the
+ * north_star's rsfg_evolve(..., n_gpus, ...)): balanced z-slabs on
+ * devices[0..n), linked halos (above), HOST buffers like rsfg_evolve.
+ * Bitwise equal to rsfg_evolve on one device.  A device may repeat (several
+ * slabs on one GPU).  Phase times in the report are host wall clock. */
+int rsfg_evolve_multi(const float* image, float* phi_inout, int32_t nx, int32_t ny, int32_t nz,
+                      const rsfg_params* p, const rsfg_options* o, const int32_t* devices, int32_t n_devices,
+                      rsfg_report* report);
 int rsfg_slab_download(rsfg_slab* s, float* phi_owned);
 int rsfg_slab_device_phi(rsfg_slab* s, float** d_phi_held);
 int64_t rsfg_slab_launches(const rsfg_slab* s);

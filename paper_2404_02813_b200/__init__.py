@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     dice,
     energy,
     evolve,
+    evolve_multi,
     evolve_step,
     extract_mask,
     gaussian_kernel,

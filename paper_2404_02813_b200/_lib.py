@@ -52,6 +52,7 @@ class rsfg_options(C.Structure):
 
 
 RSFG_STAGE_COUNT = 14
+RSFG_PEER_DESC_BYTES = 512
 
 
 class rsfg_report(C.Structure):
@@ -134,6 +135,11 @@ SIGNATURES = {
     "rsfg_state_energy": (C.c_int, [VP, FP]),
     "rsfg_state_profile": (C.c_int, [VP, I32, P(C.c_double)]),
     "rsfg_profile_name": (C.c_char_p, [I32]),
+    "rsfg_slab_peer_desc": (C.c_int, [VP, VP, I32]),
+    "rsfg_slab_link": (C.c_int, [VP, I32, VP]),
+    "rsfg_slab_step_linked": (C.c_int, [VP]),
+    "rsfg_evolve_multi": (C.c_int, [FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options), P(I32), I32,
+                                    P(rsfg_report)]),
     "rsfg_stage_name": (C.c_char_p, [I32]),
     "rsfg_stage_carrier": (C.c_int32, [I32]),
     "rsfg_state_step_profiled": (C.c_int, [VP, P(C.c_double), P(C.c_double)]),

@@ -168,6 +168,23 @@ def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, profile: Kern
     return phi[0] if squeeze else phi
 
 
+def evolve_multi(phi0, I, p: RsfParams, devices, *, fields: int = 2, report: L.rsfg_report | None = None):
+    """rsf::evolve over several GPUs of this process (rsfg_evolve_multi):
+    z-slabs on ``devices`` (a device may repeat) with peer halo links;
+    bitwise equal to ``evolve`` on one device."""
+    phi = _vol(phi0, "phi0").copy()
+    img = _vol(I, "I")
+    _check_same(phi, img, "evolve")
+    nz, ny, nx = phi.shape
+    cp = p.to_c()
+    opt = options(fields, int(devices[0]))
+    devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+    rep = report if report is not None else L.rsfg_report()
+    check(L.load().rsfg_evolve_multi(_ptr(img), _ptr(phi), nx, ny, nz, C.byref(cp), C.byref(opt), devs,
+                                     len(devices), C.byref(rep)))
+    return phi
+
+
 def extract_mask(phi, device: int = 0) -> np.ndarray:
     """rsf::extract_mask (rsf.cpp:386-396): 1 where phi < 0."""
     a = np.ascontiguousarray(phi, dtype=np.float32)

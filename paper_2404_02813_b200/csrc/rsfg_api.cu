@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -143,6 +144,21 @@ struct rsfg_slab {
   std::vector<cudaEvent_t> prof_ev;  // 2 per launch group
   std::vector<int> prof_stage;
   int prof_used = 0;
+  // Peer halo links (rsfg_slab_link): flags[side] = the last step whose halo
+  // planes on `side` have arrived (written by the neighbour after its copy).
+  unsigned int* flags = nullptr;
+  struct Link {
+    bool on = false;
+    bool ipc = false;        // pointers opened with cudaIpcOpenMemHandle (closed on release)
+    int peer_dev = 0;
+    float* phi[2] = {nullptr, nullptr};  // the neighbour's phi buffers (peer/IPC mapped)
+    unsigned int* flag = nullptr;        // the neighbour's flag word for this face
+    size_t src_off = 0, dst_off = 0, bytes = 0;
+    void* ipc_base[3] = {nullptr, nullptr, nullptr};
+  } link[2];
+  cudaStream_t push_stream = nullptr;
+  cudaEvent_t k2_done = nullptr, push_done = nullptr;
+  bool push_pending = false;
   int slot = 0;
   int iteration = 0;
   long long launches = 0;
@@ -214,6 +230,13 @@ void release(rsfg_slab* s) {
   if (s->h_counters) cudaFreeHost(s->h_counters);
   for (cudaEvent_t e : s->prof_ev) cudaEventDestroy(e);
   s->prof_ev.clear();
+  if (s->push_stream) cudaStreamSynchronize(s->push_stream), cudaStreamDestroy(s->push_stream);
+  if (s->k2_done) cudaEventDestroy(s->k2_done);
+  if (s->push_done) cudaEventDestroy(s->push_done);
+  for (auto& L : s->link)
+    for (void* b : L.ipc_base)
+      if (b) cudaIpcCloseMemHandle(b);
+  cudaFree(s->flags);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -437,6 +460,8 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&s->flags, 2 * sizeof(unsigned int)));
+  CUDA_TRY(cudaMemsetAsync(s->flags, 0, 2 * sizeof(unsigned int), s->stream));
   if (s->fast && s->fields == 2 && s->t2.r == 0 && (s->nx % 4) == 0)
     CUDA_TRY(cudaMalloc(&s->hh, held * sizeof(float2)));
   make_xy_maps(s);
@@ -1256,6 +1281,10 @@ __attribute__((visibility("default"))) int rsfg_slab_set_stream(rsfg_slab* s, vo
   return RSFG_OK;
 }
 
+namespace {
+int enable_peer(int from, int to);
+}
+
 __attribute__((visibility("default"))) int rsfg_slab_exchange(rsfg_slab* lo, rsfg_slab* hi) {
   if (!lo || !hi) return fail(RSFG_ERR_STATE, "null slab");
   if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->nz != hi->nz)
@@ -1265,6 +1294,10 @@ __attribute__((visibility("default"))) int rsfg_slab_exchange(rsfg_slab* lo, rsf
   rsfg_slab_halo(lo, 1, &lo_send, &lo_recv, &lo_bytes);
   rsfg_slab_halo(hi, 0, &hi_send, &hi_recv, &hi_bytes);
   if (lo_bytes != hi_bytes) return fail(RSFG_ERR_SHAPE, "halo sizes differ across the face");
+  if (lo->dev != hi->dev) {  // direct NVLink copies instead of staging through the host
+    if (int rc = enable_peer(lo->dev, hi->dev)) return rc;
+    if (int rc = enable_peer(hi->dev, lo->dev)) return rc;
+  }
   cudaEvent_t e_hi, e_lo;
   CUDA_TRY(cudaSetDevice(hi->dev));
   CUDA_TRY(cudaEventCreateWithFlags(&e_hi, cudaEventDisableTiming));
@@ -1326,6 +1359,318 @@ __attribute__((visibility("default"))) void rsfg_slab_destroy(rsfg_slab* s) {
   delete s;
 }
 
+
+// ------------------------------------------------------- peer halo links
+namespace {
+// What a neighbour needs to push into this slab: geometry, the two phi
+// buffers and the flag words -- raw pointers (same process) or CUDA IPC
+// handles (another process on this node).
+struct PeerDesc {
+  uint32_t magic, version;
+  int32_t dev, nx, ny, nz, z0, z1, zb, ze, ipc, pad;
+  uint64_t phi[2], flags;
+  cudaIpcMemHandle_t h_phi[2], h_flags;
+};
+static_assert(sizeof(PeerDesc) <= RSFG_PEER_DESC_BYTES, "descriptor too large");
+constexpr uint32_t kDescMagic = 0x52534647u;  // "RSFG"
+
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (WaitValueFn) nullptr;
+    return reinterpret_cast<WaitValueFn>(f);
+  }();
+  return fn;
+}
+
+// The slab's stream waits until flags[side] >= v (halo of step v arrived).
+int wait_flag(rsfg_slab* s, int side, unsigned int v) {
+  static const bool no_memops = std::getenv("RSFG_NO_STREAM_MEMOPS") != nullptr;
+  WaitValueFn fn = no_memops ? nullptr : wait_value_fn();
+  if (fn && fn((CUstream)s->stream, (CUdeviceptr)(s->flags + side), v, CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS)
+    return RSFG_OK;
+  s->launches += rsfg::launch_flag_wait(s->flags + side, v, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  return RSFG_OK;
+}
+
+int enable_peer(int from, int to) {
+  if (from == to) return RSFG_OK;
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, from, to));
+  if (!can) return fail(RSFG_ERR_COMM, "no peer access from device " + std::to_string(from) + " to " + std::to_string(to));
+  CUDA_TRY(cudaSetDevice(from));
+  cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else if (e != cudaSuccess) return fail(RSFG_ERR_COMM, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+  return RSFG_OK;
+}
+
+// One step with linked faces: interior xy work, wait for the halos of this
+// step, finish (kernel 2 -> phi'), then push the new boundary planes into the
+// neighbours' halos and bump their flags on a side stream that overlaps the
+// next step's interior work.
+int step_linked(rsfg_slab* s) {
+  if (int rc = step_interior(s)) return rc;
+  const unsigned int it = (unsigned int)s->iteration;
+  for (int side = 0; side < 2; ++side)
+    if (s->link[side].on)
+      if (int rc = wait_flag(s, side, it)) return rc;
+  // the previous push read the buffer this step's successor will overwrite
+  if (s->push_pending) CUDA_TRY(cudaStreamWaitEvent(s->stream, s->push_done, 0));
+  if (int rc = step_finish(s, rsfg::kUpdate, s->phi[s->cur ^ 1])) return rc;
+  if (!s->link[0].on && !s->link[1].on) return RSFG_OK;
+  CUDA_TRY(cudaEventRecord(s->k2_done, s->stream));
+  CUDA_TRY(cudaStreamWaitEvent(s->push_stream, s->k2_done, 0));
+  for (int side = 0; side < 2; ++side) {
+    const rsfg_slab::Link& L = s->link[side];
+    if (!L.on) continue;
+    CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(L.phi[s->cur]) + L.dst_off,
+                             reinterpret_cast<const char*>(s->phi[s->cur]) + L.src_off, L.bytes, cudaMemcpyDefault,
+                             s->push_stream));
+    s->launches += rsfg::launch_flag_store(L.flag, (unsigned int)s->iteration, s->push_stream);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(s->push_done, s->push_stream));
+  s->push_pending = true;
+  return RSFG_OK;
+}
+
+// Counters of the last k steps without formatting: sign changes of the last
+// step, the earliest (1-based) iteration with a non-finite value and its
+// smallest global index (0 / -1 if none).
+int read_counters(rsfg_slab* s, int k, long long* last_sc, int* bad_it, long long* bad_idx) {
+  CUDA_TRY(cudaSetDevice(s->dev));
+  CUDA_TRY(cudaMemcpyAsync(s->h_counters, s->counters, kSlots * 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  *bad_it = 0;
+  *bad_idx = -1;
+  for (int i = k; i >= 1; --i) {
+    const int sl = ((s->slot - i) % kSlots + kSlots) % kSlots;
+    if (i == 1) *last_sc = (long long)s->h_counters[2 * sl];
+    const unsigned long long bad = s->h_counters[2 * sl + 1];
+    if (bad != ~0ull && *bad_it == 0) {
+      *bad_it = s->iteration - i + 1;
+      *bad_idx = (long long)bad;
+    }
+  }
+  return RSFG_OK;
+}
+}  // namespace
+
+__attribute__((visibility("default"))) int rsfg_slab_peer_desc(rsfg_slab* s, void* desc, int32_t ipc) {
+  if (!s || !desc) return fail(RSFG_ERR_STATE, "null argument");
+  PeerDesc d{};
+  d.magic = kDescMagic;
+  d.version = 1;
+  d.dev = s->dev;
+  d.nx = s->nx, d.ny = s->ny, d.nz = s->nz, d.z0 = s->z0, d.z1 = s->z1, d.zb = s->zb, d.ze = s->ze;
+  d.ipc = ipc ? 1 : 0;
+  d.phi[0] = (uint64_t)(uintptr_t)s->phi[0];
+  d.phi[1] = (uint64_t)(uintptr_t)s->phi[1];
+  d.flags = (uint64_t)(uintptr_t)s->flags;
+  if (ipc) {
+    CUDA_TRY(cudaSetDevice(s->dev));
+    CUDA_TRY(cudaIpcGetMemHandle(&d.h_phi[0], s->phi[0]));
+    CUDA_TRY(cudaIpcGetMemHandle(&d.h_phi[1], s->phi[1]));
+    CUDA_TRY(cudaIpcGetMemHandle(&d.h_flags, s->flags));
+  }
+  std::memset(desc, 0, RSFG_PEER_DESC_BYTES);
+  std::memcpy(desc, &d, sizeof d);
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_link(rsfg_slab* s, int32_t side, const void* desc) {
+  if (!s || !desc || (side != 0 && side != 1)) return fail(RSFG_ERR_STATE, "bad argument");
+  PeerDesc d;
+  std::memcpy(&d, desc, sizeof d);
+  if (d.magic != kDescMagic || d.version != 1) return fail(RSFG_ERR_STATE, "not a peer descriptor");
+  if (d.nx != s->nx || d.ny != s->ny || d.nz != s->nz || (side == 0 ? d.z1 != s->z0 : d.z0 != s->z1))
+    return fail(RSFG_ERR_SHAPE, "peer slab is not the z-neighbour on that face");
+  rsfg_slab::Link& L = s->link[side];
+  if (L.on) return fail(RSFG_ERR_STATE, "face already linked");
+  CUDA_TRY(cudaSetDevice(s->dev));
+  if (d.ipc) {
+    void* p[3];
+    const cudaIpcMemHandle_t* h[3] = {&d.h_phi[0], &d.h_phi[1], &d.h_flags};
+    for (int i = 0; i < 3; ++i) {
+      cudaError_t e = cudaIpcOpenMemHandle(&p[i], *h[i], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(p[j]);
+        return fail(RSFG_ERR_COMM, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      L.ipc_base[i] = p[i];
+    }
+    L.phi[0] = static_cast<float*>(p[0]);
+    L.phi[1] = static_cast<float*>(p[1]);
+    L.flag = static_cast<unsigned int*>(p[2]);
+    L.ipc = true;
+  } else {
+    if (int rc = enable_peer(s->dev, d.dev)) return rc;
+    CUDA_TRY(cudaSetDevice(s->dev));
+    L.phi[0] = reinterpret_cast<float*>((uintptr_t)d.phi[0]);
+    L.phi[1] = reinterpret_cast<float*>((uintptr_t)d.phi[1]);
+    L.flag = reinterpret_cast<unsigned int*>((uintptr_t)d.flags);
+  }
+  const size_t plane = (size_t)s->nx * s->ny * sizeof(float);
+  if (side == 1) {  // neighbour above: its halo planes [d.zb, d.z0) are our owned planes
+    L.flag += 0;    // it receives on its side 0
+    L.src_off = s->off(d.zb) * sizeof(float);
+    L.dst_off = 0;
+    L.bytes = (size_t)(d.z0 - d.zb) * plane;
+  } else {          // neighbour below: its halo planes [d.z1, d.ze)
+    L.flag += 1;
+    L.src_off = s->off(s->z0) * sizeof(float);
+    L.dst_off = (size_t)(d.z1 - d.zb) * plane;
+    L.bytes = (size_t)(d.ze - d.z1) * plane;
+  }
+  if (d.zb < s->zb && side == 1) return fail(RSFG_ERR_SHAPE, "neighbour halo exceeds this slab");
+  L.peer_dev = d.dev;
+  L.on = true;
+  if (!s->push_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->push_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->k2_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->push_done, cudaEventDisableTiming));
+  }
+  return RSFG_OK;
+}
+
+__attribute__((visibility("default"))) int rsfg_slab_step_linked(rsfg_slab* s) {
+  if (!s) return fail(RSFG_ERR_STATE, "null slab");
+  return step_linked(s);
+}
+
+// rsf::evolve over several GPUs of this process: z-slabs on
+// devices[0..n), halos pushed over peer memory (NVLink) every step; bitwise
+// equal to rsfg_evolve on one device.
+__attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image, float* phi, int32_t nx, int32_t ny,
+                                                             int32_t nz, const rsfg_params* p, const rsfg_options* o,
+                                                             const int32_t* devices, int32_t n_devices,
+                                                             rsfg_report* rep) {
+  rsfg_report local{};
+  if (!rep) rep = &local;
+  std::memset(rep, 0, sizeof *rep);
+  if (int rc = validate(p)) return rc;
+  if (!image || !phi || !devices || n_devices < 1) return fail(RSFG_ERR_STATE, "null argument");
+  rsfg_options opt;
+  rsfg_options_default(&opt);
+  if (o) opt = *o;
+  if (n_devices == 1 || nz == 1) {
+    opt.device = devices[0];
+    return rsfg_evolve(image, phi, nx, ny, nz, p, &opt, nullptr, nullptr, 0, rep);
+  }
+  rsfg::Taps t1, t2;
+  if (int rc = make_taps(p->sigma1, t1)) return rc;
+  if (int rc = make_taps(p->sigma2, t2)) return rc;
+  const int h = std::max(std::max(t1.r, t2.r), 2);
+  const int n = n_devices;
+  if (nz / n < h)
+    return fail(RSFG_ERR_SHAPE, "nz=" + std::to_string(nz) + " over " + std::to_string(n) +
+                                    " slabs leaves a slab thinner than the halo (" + std::to_string(h) + ")");
+  std::vector<rsfg_slab*> sl(n, nullptr);
+  struct Guard {
+    std::vector<rsfg_slab*>& v;
+    ~Guard() {
+      for (rsfg_slab* s : v)
+        if (s) release(s), delete s;
+    }
+  } guard{sl};
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  const size_t plane = (size_t)nx * ny;
+  int z = 0;
+  for (int i = 0; i < n; ++i) {  // balanced ranges (spmd.plan_slabs)
+    const int cnt = nz / n + (i < nz % n ? 1 : 0);
+    rsfg_options oi = opt;
+    oi.device = devices[i];
+    sl[i] = new rsfg_slab;
+    if (int rc = setup(sl[i], nx, ny, nz, z, z + cnt, p, &oi)) return rc;
+    if (int rc = upload(sl[i], phi + (size_t)sl[i]->zb * plane, image + (size_t)sl[i]->zb * plane,
+                        cudaMemcpyHostToDevice))
+      return rc;
+    z += cnt;
+  }
+  float lo = 0.f, hi = 0.f;
+  for (int i = 0; i < n; ++i) {
+    float a, b;
+    if (int rc = local_range(sl[i], &a, &b)) return rc;
+    lo = i ? std::min(lo, a) : a;
+    hi = i ? std::max(hi, b) : b;
+  }
+  const auto t1c = clk::now();
+  for (int i = 0; i < n; ++i)
+    if (int rc = init_static(sl[i], lo, hi)) return rc;
+  char desc[RSFG_PEER_DESC_BYTES];
+  for (int i = 0; i < n; ++i) {
+    if (i > 0) {
+      if (int rc = rsfg_slab_peer_desc(sl[i - 1], desc, 0)) return rc;
+      if (int rc = rsfg_slab_link(sl[i], 0, desc)) return rc;
+    }
+    if (i + 1 < n) {
+      if (int rc = rsfg_slab_peer_desc(sl[i + 1], desc, 0)) return rc;
+      if (int rc = rsfg_slab_link(sl[i], 1, desc)) return rc;
+    }
+  }
+  for (int i = 0; i < n; ++i) CUDA_TRY(cudaStreamSynchronize(sl[i]->stream));
+  const auto t2c = clk::now();
+  const bool per_step = p->convergence_fraction > 0.0;
+  const int check_every = sl[0]->check_every;
+  long long l0 = 0;
+  for (rsfg_slab* s : sl) l0 += s->launches;
+  int pending = 0;
+  for (int it = 0; it < p->max_iters; ++it) {
+    for (rsfg_slab* s : sl)
+      if (int rc = step_linked(s)) return rc;
+    ++pending;
+    if (per_step || pending == check_every || it + 1 == p->max_iters) {
+      long long sc_all = 0, best_idx = -1;
+      int best_it = 0;
+      for (rsfg_slab* s : sl) {
+        long long sc = 0, bidx = -1;
+        int bit = 0;
+        if (int rc = read_counters(s, pending, &sc, &bit, &bidx)) return rc;
+        sc_all += sc;
+        if (bit && (!best_it || bit < best_it || (bit == best_it && bidx < best_idx))) best_it = bit, best_idx = bidx;
+      }
+      pending = 0;
+      rep->iterations = it + 1;
+      rep->last_sign_change_fraction = (double)sc_all / ((double)nx * ny * nz);
+      if (best_it) {
+        const int x = (int)(best_idx % nx), y = (int)((best_idx / nx) % ny), zz = (int)(best_idx / (long long)plane);
+        char buf[160];
+        snprintf(buf, sizeof buf, "evolution produced a non-finite value at voxel (%d,%d,%d), iteration %d", x, y, zz,
+                 best_it);
+        rep->blowup_iteration = best_it;
+        rep->blowup_x = x, rep->blowup_y = y, rep->blowup_z = zz;
+        return fail(RSFG_ERR_BLOWUP, buf);
+      }
+      if (per_step && rep->last_sign_change_fraction < p->convergence_fraction) break;  // rsf.cpp:378
+    }
+  }
+  for (rsfg_slab* s : sl) CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const auto t3c = clk::now();
+  for (rsfg_slab* s : sl) {
+    CUDA_TRY(cudaSetDevice(s->dev));
+    CUDA_TRY(cudaMemcpyAsync(phi + (size_t)s->z0 * plane, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float),
+                             cudaMemcpyDeviceToHost, s->stream));
+  }
+  for (rsfg_slab* s : sl) CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const auto t4c = clk::now();
+  auto ms = [](clk::duration d) { return std::chrono::duration<double, std::milli>(d).count(); };
+  rep->ms_h2d = ms(t1c - t0);
+  rep->ms_init = ms(t2c - t1c);
+  rep->ms_loop = ms(t3c - t2c);
+  rep->ms_d2h = ms(t4c - t3c);
+  long long l1 = 0;
+  for (rsfg_slab* s : sl) l1 += s->launches;
+  rep->gpu_launches = l1 - l0;
+  return RSFG_OK;
+}
 
 __attribute__((visibility("default"))) void rsfg_blob_params_default(rsfg_blob_params* b) {
   if (!b) return;

@@ -145,6 +145,15 @@ int gaussian_taps(double sigma, Taps& t);
 // planes of g): x a->b, y b->a, z a->b; the result is left in b.
 int launch_conv_pair(const Geom& g, const Taps& t, float2* a, float2* b, cudaStream_t st);
 
+// Peer halo links (rsfg_api.cu, rsfg_slab_link): after a step, a slab copies
+// its boundary phi' planes into the neighbour's halo (peer memory over NVLink
+// or the same device) and then stores the step number into the neighbour's
+// flag word; the neighbour's stream waits for flag >= its step before the
+// halo-dependent work.  flag_wait is the kernel fallback for
+// cuStreamWaitValue32.
+int launch_flag_store(unsigned int* flag, unsigned int v, cudaStream_t st);
+int launch_flag_wait(const unsigned int* flag, unsigned int v, cudaStream_t st);
+
 // phi0 initialisation (rsfg_seed.cu; reference seeding.cpp:83-235).
 struct SeedHost {
   int x, y, z;

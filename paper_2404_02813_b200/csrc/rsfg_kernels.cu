@@ -203,3 +203,33 @@ int launch_mask(const float* phi, float* mask, long long n, cudaStream_t st) {
 }
 
 }  // namespace rsfg
+
+// ------------------------------------------------------------ peer halo flags
+namespace rsfg {
+namespace {
+// Publishes "the halo planes of step v have landed" into a (possibly peer)
+// flag word; the preceding copy on the same stream is complete when this runs.
+__global__ void flag_store_kernel(unsigned int* flag, unsigned int v) {
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned int*>(flag) = v;
+  __threadfence_system();
+}
+
+// Fallback wait when stream memory operations are unavailable: one thread
+// polls the local flag word until it reaches v.
+__global__ void flag_wait_kernel(const unsigned int* flag, unsigned int v) {
+  while (*reinterpret_cast<const volatile unsigned int*>(flag) < v) __nanosleep(200);
+  __threadfence_system();
+}
+}  // namespace
+
+int launch_flag_store(unsigned int* flag, unsigned int v, cudaStream_t st) {
+  flag_store_kernel<<<1, 1, 0, st>>>(flag, v);
+  return 1;
+}
+
+int launch_flag_wait(const unsigned int* flag, unsigned int v, cudaStream_t st) {
+  flag_wait_kernel<<<1, 1, 0, st>>>(flag, v);
+  return 1;
+}
+}  // namespace rsfg

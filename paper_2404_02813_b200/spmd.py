@@ -103,6 +103,20 @@ class Slab:
     def step_finish(self):
         check(self.lib.rsfg_slab_step_finish(self.h))
 
+    def peer_desc(self, ipc: bool) -> bytes:
+        """This slab's link descriptor (rsfg_slab_peer_desc): raw device
+        pointers (ipc=False, same process) or CUDA IPC handles (ipc=True)."""
+        buf = C.create_string_buffer(L.RSFG_PEER_DESC_BYTES)
+        check(self.lib.rsfg_slab_peer_desc(self.h, buf, 1 if ipc else 0))
+        return buf.raw
+
+    def link(self, side: int, desc: bytes):
+        buf = C.create_string_buffer(desc, L.RSFG_PEER_DESC_BYTES)
+        check(self.lib.rsfg_slab_link(self.h, side, buf))
+
+    def step_linked(self):
+        check(self.lib.rsfg_slab_step_linked(self.h))
+
     def counters(self):
         sc, bad = C.c_int64(), C.c_int64()
         check(self.lib.rsfg_slab_counters(self.h, C.byref(sc), C.byref(bad)))
@@ -129,9 +143,15 @@ class Slab:
 
 
 class SlabSet:
-    """P slabs in one process (one or several local GPUs)."""
+    """P slabs in one process (one or several local GPUs).
 
-    def __init__(self, phi0, I, p: RsfParams, parts: int, *, fields=2, devices=None, check_every=25):
+    linked=False: halos move with rsfg_slab_exchange between the interior and
+    finish halves of every step.  linked=True: peer halo links
+    (rsfg_slab_link) -- each slab pushes its boundary planes into its
+    neighbours' halos after its step and bumps their flags; no host sync."""
+
+    def __init__(self, phi0, I, p: RsfParams, parts: int, *, fields=2, devices=None, check_every=25,
+                 linked=False):
         nz, ny, nx = phi0.shape
         self.nx, self.ny = nx, ny
         self.check_every = max(1, check_every)
@@ -147,9 +167,21 @@ class SlabSet:
         lo, hi = min(los), max(his)  # global [min I, max I] (volume.cpp:25-33)
         for s in self.slabs:
             s.init(lo, hi)
+        self.linked = linked
+        if linked:
+            for a, b in zip(self.slabs, self.slabs[1:]):
+                a.link(1, b.peer_desc(False))
+                b.link(0, a.peer_desc(False))
 
     def step(self):
         lib = L.load()
+        if self.linked:
+            for s in self.slabs:
+                s.step_linked()
+            self.iteration += 1
+            if self.iteration % self.check_every == 0:
+                self.check_blowup()
+            return
         for s in self.slabs:
             s.step_interior()
         for a, b in zip(self.slabs, self.slabs[1:]):
@@ -210,7 +242,13 @@ class _DevView:
 class DistSlab:
     """One slab per rank; halo exchange with torch.distributed (NCCL on GPUs).
 
-    transport="device" (default) posts NCCL send/recv on views of the slab's own
+    transport="ipc" is the B200-native data path: peer halo links over CUDA IPC
+    (rsfg_slab_link) -- each rank copies its boundary planes straight into its
+    neighbours' halo rows over NVLink and bumps their flag words; the process
+    group only carries the one-time descriptor exchange and the scalar
+    reductions.  It also runs with several ranks on one GPU (IPC between
+    processes on the same device), which is how it is tested here.
+    transport="device" posts NCCL send/recv on views of the slab's own
     device buffers, overlapped with the interior work.  transport="host" stages
     the halo planes through host memory for CPU-only process groups (gloo): it
     lets several ranks share one GPU, which is how this path is tested on
@@ -236,10 +274,20 @@ class DistSlab:
         self.stream = torch.cuda.current_stream()
         self.slab.set_stream(self.stream.cuda_stream)
         self.transport = transport
+        self.red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
         lo, hi = self.slab.local_range()
-        t = torch.tensor([-lo, hi], dtype=torch.float32, device="cuda" if transport == "device" else "cpu")
+        t = torch.tensor([-lo, hi], dtype=torch.float32, device=self.red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         self.slab.init(-float(t[0]), float(t[1]))
+        if transport == "ipc":
+            descs = [None] * self.world
+            dist.all_gather_object(descs, self.slab.peer_desc(True))
+            if self.rank > 0:
+                self.slab.link(0, descs[self.rank - 1])
+            if self.rank < self.world - 1:
+                self.slab.link(1, descs[self.rank + 1])
+            torch.cuda.synchronize(dev)
+            dist.barrier()
 
     def _views(self, side):
         send, recv, n = self.slab.halo_views(side)
@@ -249,7 +297,9 @@ class DistSlab:
         return t.as_tensor(_DevView(send, n), device="cuda"), t.as_tensor(_DevView(recv, n), device="cuda")
 
     def step(self):
-        if self.transport == "host":
+        if self.transport == "ipc":
+            self.slab.step_linked()
+        elif self.transport == "host":
             self._step_host()
         else:
             reqs = start_halo_exchange(self.dist, self.rank, self.world, self._views(0), self._views(1))
@@ -267,8 +317,7 @@ class DistSlab:
         t = self.torch
         _, bad = self.slab.counters()
         big = t.iinfo(t.int64).max
-        v = t.tensor([bad if bad >= 0 else big], dtype=t.int64,
-                     device="cuda" if self.transport == "device" else "cpu")
+        v = t.tensor([bad if bad >= 0 else big], dtype=t.int64, device=self.red_dev)
         self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN)
         g = int(v.item())
         if g != big:

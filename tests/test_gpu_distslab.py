@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _worker(rank, world, port, phi0, img, steps, sigma1, q):
+def _worker(rank, world, port, phi0, img, steps, sigma1, q, transport="host"):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -27,7 +27,7 @@ def _worker(rank, world, port, phi0, img, steps, sigma1, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ds = DistSlab(phi0, img, rsf.RsfParams(sigma1=sigma1), transport="host")
+        ds = DistSlab(phi0, img, rsf.RsfParams(sigma1=sigma1), transport=transport)
         for _ in range(steps):
             ds.step()
         torch.cuda.synchronize()
@@ -36,16 +36,21 @@ def _worker(rank, world, port, phi0, img, steps, sigma1, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape", [(2, (96, 28, 80)), (3, (40, 36, 48))])
-def test_distslab_bitwise_vs_monolithic(world, shape):
+@pytest.mark.parametrize("world,shape,transport", [(2, (96, 28, 80), "host"), (3, (40, 36, 48), "host"),
+                                                   (2, (96, 28, 80), "ipc"), (3, (64, 40, 48), "ipc")])
+def test_distslab_bitwise_vs_monolithic(world, shape, transport):
+    """transport="ipc": the peer-link data path across processes (CUDA IPC
+    handles of each rank's phi buffers and flag words; on one GPU the
+    "peers" are other processes on the same device)."""
     import paper_2404_02813_b200 as rsf
     img, phi, _ = case(*shape)
     img, phi = np.array(img), np.array(phi)
-    steps, sigma1 = 4, 3.0
+    steps, sigma1 = 6, 3.0
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 2000)
-    procs = [ctx.Process(target=_worker, args=(r, world, port, phi, img, steps, sigma1, q)) for r in range(world)]
+    port = 29500 + (os.getpid() % 1000) * 8 + world + (4 if transport == "ipc" else 0)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, phi, img, steps, sigma1, q, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     parts = [q.get(timeout=300) for _ in range(world)]

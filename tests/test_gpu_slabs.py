@@ -52,6 +52,46 @@ def test_slab_generic_radius_bitwise():
     assert np.array_equal(ss.phi(), st.phi)
 
 
+@pytest.mark.parametrize("parts,fields,sigma1", [(2, 2, 3.0), (3, 4, 3.0), (4, 2, 2.0), (2, 2, 7.0)])
+def test_linked_slabs_bitwise(parts, fields, sigma1):
+    """Peer halo links (rsfg_slab_link / step_linked): pushes of the boundary
+    planes + flag waits, no host synchronisation, several slabs on one GPU."""
+    import paper_2404_02813_b200 as rsf
+    from paper_2404_02813_b200.spmd import SlabSet
+    img, phi, _ = case(96, 28, 80)
+    p = rsf.RsfParams(sigma1=sigma1)
+    st = rsf.init_evolution(phi, img, p, fields=fields)
+    ss = SlabSet(np.array(phi), np.array(img), p, parts, fields=fields, linked=True)
+    for _ in range(7):
+        st.step()
+        ss.step()
+    assert np.array_equal(ss.phi(), st.phi)
+    ss.close()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_evolve_multi_bitwise(n):
+    """rsfg_evolve_multi (the C-ABI multi-GPU entry; one device repeated here)."""
+    import paper_2404_02813_b200 as rsf
+    img, phi, _ = case(64, 48, 40, n_branches=4)
+    p = rsf.RsfParams(sigma1=3.0, max_iters=30)
+    rep = rsf._lib.rsfg_report()
+    got = rsf.evolve_multi(phi, img, p, [0] * n, report=rep)
+    assert np.array_equal(got, rsf.evolve(phi, img, p))
+    assert rep.iterations == 30 and rep.gpu_launches > 0
+
+
+def test_evolve_multi_blowup_and_thin():
+    import paper_2404_02813_b200 as rsf
+    img, phi, _ = case(40, 36, 32)
+    bad = np.array(phi)
+    bad[20, 5, 7] = np.nan
+    with pytest.raises(rsf.BlowupError, match=r"voxel \(7,5,20\), iteration 1"):
+        rsf.evolve_multi(bad, img, rsf.RsfParams(sigma1=2.0, max_iters=5), [0, 0])
+    with pytest.raises(rsf.ShapeError):
+        rsf.evolve_multi(phi, img, rsf.RsfParams(sigma1=3.0, max_iters=5), [0] * 8)
+
+
 def test_thin_slab_rejected():
     import paper_2404_02813_b200 as rsf
     from paper_2404_02813_b200.spmd import plan_slabs
