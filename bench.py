@@ -324,23 +324,25 @@ def bench_single(args):
                 times.append(dt)
         return nvox * ITERS_CFG / statistics.median(times), rep2
 
-    page_img, page_phi = np.array(img), np.empty_like(phi0)  # ordinary (pageable) host memory
-    e2e_page, rep_page = e2e_run(page_phi, page_img)
-    phi_gpu_final = page_phi.copy()
-    t_img = torch.from_numpy(img).pin_memory()
-    t_phi = torch.empty_like(t_img).pin_memory()
-    e2e_pin, rep_pin = e2e_run(t_phi.numpy(), t_img.numpy())
-    del t_img, t_phi
-
     def phases(r):
         return {"h2d": round(r.ms_h2d, 2), "init": round(r.ms_init, 2), "loop": round(r.ms_loop, 2),
                 "d2h": round(r.ms_d2h, 2)}
 
-    e2e = {"value": e2e_page, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
-           "iterations_per_step": ITERS_CFG, "host_memory": "pageable (numpy / std::vector, as tiling.cpp:251)",
-           "api": "rsfg_evolve (host buffers; device workspace allocated and freed inside every call)",
-           "phase_ms": phases(rep_page),
-           "pinned": {"value": e2e_pin, "phase_ms": phases(rep_pin)}}
+    e2e = None
+    phi_gpu_final = None
+    if args.e2e_steps > 0:
+        page_img, page_phi = np.array(img), np.empty_like(phi0)  # ordinary (pageable) host memory
+        e2e_page, rep_page = e2e_run(page_phi, page_img)
+        phi_gpu_final = page_phi.copy()
+        t_img = torch.from_numpy(img).pin_memory()
+        t_phi = torch.empty_like(t_img).pin_memory()
+        e2e_pin, rep_pin = e2e_run(t_phi.numpy(), t_img.numpy())
+        del t_img, t_phi
+        e2e = {"value": e2e_page, "unit": UNIT, "h2d_bytes_per_step": 2 * nvox * 4, "d2h_bytes_per_step": nvox * 4,
+               "iterations_per_step": ITERS_CFG, "host_memory": "pageable (numpy / std::vector, as tiling.cpp:251)",
+               "api": "rsfg_evolve (host buffers; device workspace allocated and freed inside every call)",
+               "phase_ms": phases(rep_page),
+               "pinned": {"value": e2e_pin, "phase_ms": phases(rep_pin)}}
 
     # ---- CPU baseline + parity: the reference itself on the same 512^3 volume
     cpu, parity = None, None
@@ -358,7 +360,8 @@ def bench_single(args):
             parity = {"cfg2_step1": {"max_abs_dphi": float(d.max()),
                                      "max_rel_dphi": float((d / np.maximum(1.0, np.abs(ref_phi1))).max()),
                                      "gate": "P1 max|dphi| <= 1e-4 (SURVEY.md 8(c))"},
-                      "cfg2_200it_gpu_dice_vs_gt": rsf.dice(phi_gpu_final < 0, gt > 0.5)}
+                      "cfg2_200it_gpu_dice_vs_gt": (rsf.dice(phi_gpu_final < 0, gt > 0.5)
+                                                    if phi_gpu_final is not None else None)}
             if not args.no_parity:
                 parity["cfg1_100it"] = parity_cfg1(reference_lib())
         except Exception as e:  # reference build missing on this host

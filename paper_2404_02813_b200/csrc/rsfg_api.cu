@@ -504,6 +504,11 @@ int upload(rsfg_slab* s, const float* phi, const float* image, cudaMemcpyKind ki
   CUDA_TRY(cudaSetDevice(s->dev));
   s->hh_valid = false;
   const size_t bytes = s->held() * sizeof(float);
+  if (kind == cudaMemcpyHostToDevice) {  // caller memory, pageable or pinned
+    CUDA_TRY(rsfg::copy_h2d(s->phi[s->cur], phi, bytes, s->stream));
+    CUDA_TRY(rsfg::copy_h2d(s->image, image, bytes, s->stream));
+    return RSFG_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, bytes, kind, s->stream));
   CUDA_TRY(cudaMemcpyAsync(s->image, image, bytes, kind, s->stream));
   return RSFG_OK;
@@ -915,8 +920,7 @@ __attribute__((visibility("default"))) int rsfg_state_read_phi(rsfg_state* st, f
   if (!st || !phi) return fail(RSFG_ERR_STATE, "null argument");
   rsfg_slab* s = &st->e;
   CUDA_TRY(cudaSetDevice(s->dev));
-  CUDA_TRY(cudaMemcpyAsync(phi, s->phi[s->cur], s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  CUDA_TRY(rsfg::copy_d2h(phi, s->phi[s->cur], s->held() * sizeof(float), s->stream));
   return RSFG_OK;
 }
 
@@ -924,7 +928,7 @@ __attribute__((visibility("default"))) int rsfg_state_write_phi(rsfg_state* st, 
   if (!st || !phi) return fail(RSFG_ERR_STATE, "null argument");
   rsfg_slab* s = &st->e;
   CUDA_TRY(cudaSetDevice(s->dev));
-  CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, s->held() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(rsfg::copy_h2d(s->phi[s->cur], phi, s->held() * sizeof(float), s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->valid = true;
   s->hh_valid = false;
@@ -1072,13 +1076,13 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
   const size_t held_bytes = s->held() * sizeof(float);
   s->hh_valid = false;
   cudaEventRecord(ev[0], s->stream);
-  CUDA_TRY(cudaMemcpyAsync(s->image, image, held_bytes, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(rsfg::copy_h2d(s->image, image, held_bytes, s->stream));
   cudaEventRecord(ev[1], s->stream);
   float lo, hi;
   if (int rc = local_range(s, &lo, &hi)) return rc;
   if (int rc = init_static(s, lo, hi)) return rc;
   CUDA_TRY(cudaStreamWaitEvent(side, ev[0], 0));  // after setup's memsets of phi[]
-  CUDA_TRY(cudaMemcpyAsync(s->phi[s->cur], phi, held_bytes, cudaMemcpyHostToDevice, side));
+  CUDA_TRY(rsfg::copy_h2d(s->phi[s->cur], phi, held_bytes, side));
   CUDA_TRY(cudaEventRecord(phi_up, side));
   CUDA_TRY(cudaStreamWaitEvent(s->stream, phi_up, 0));
   cudaEventRecord(ev[2], s->stream);
@@ -1124,7 +1128,7 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
     }
   }
   cudaEventRecord(ev[3], s->stream);
-  CUDA_TRY(cudaMemcpyAsync(phi, s->phi[s->cur], s->held() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(rsfg::copy_d2h(phi, s->phi[s->cur], s->held() * sizeof(float), s->stream));
   cudaEventRecord(ev[4], s->stream);
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   float ms;
@@ -1339,9 +1343,7 @@ __attribute__((visibility("default"))) int rsfg_slab_counters(rsfg_slab* s, int6
 __attribute__((visibility("default"))) int rsfg_slab_download(rsfg_slab* s, float* phi_owned) {
   if (!s || !phi_owned) return fail(RSFG_ERR_STATE, "null argument");
   CUDA_TRY(cudaSetDevice(s->dev));
-  CUDA_TRY(cudaMemcpyAsync(phi_owned, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float),
-                           cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  CUDA_TRY(rsfg::copy_d2h(phi_owned, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float), s->stream));
   return RSFG_OK;
 }
 
@@ -1656,10 +1658,9 @@ __attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image,
   const auto t3c = clk::now();
   for (rsfg_slab* s : sl) {
     CUDA_TRY(cudaSetDevice(s->dev));
-    CUDA_TRY(cudaMemcpyAsync(phi + (size_t)s->z0 * plane, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float),
-                             cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(rsfg::copy_d2h(phi + (size_t)s->z0 * plane, s->phi[s->cur] + s->off(s->z0), s->owned() * sizeof(float),
+                            s->stream));
   }
-  for (rsfg_slab* s : sl) CUDA_TRY(cudaStreamSynchronize(s->stream));
   const auto t4c = clk::now();
   auto ms = [](clk::duration d) { return std::chrono::duration<double, std::milli>(d).count(); };
   rep->ms_h2d = ms(t1c - t0);

@@ -154,6 +154,14 @@ int launch_conv_pair(const Geom& g, const Taps& t, float2* a, float2* b, cudaStr
 int launch_flag_store(unsigned int* flag, unsigned int v, cudaStream_t st);
 int launch_flag_wait(const unsigned int* flag, unsigned int v, cudaStream_t st);
 
+// Host<->device copies of caller memory (rsfg_stage.cu): pageable buffers go
+// through a pinned chunk ring filled/drained by several host threads; pinned
+// ones go straight to the DMA engine.  Both return when the caller's buffer
+// may be reused (copy_d2h: when the data has landed).
+bool host_is_pinned(const void* p);
+cudaError_t copy_h2d(void* dst, const void* src, size_t n, cudaStream_t st);
+cudaError_t copy_d2h(void* dst, const void* src, size_t n, cudaStream_t st);
+
 // phi0 initialisation (rsfg_seed.cu; reference seeding.cpp:83-235).
 struct SeedHost {
   int x, y, z;

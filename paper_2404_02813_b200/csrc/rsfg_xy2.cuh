@@ -489,12 +489,42 @@ int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* 
 // kernel 1 tile height used by xy2 (RSFG_XY2_TY overrides: 32 or 64)
 constexpr int kXY2DefaultTY = 32;
 
-#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6)
+#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 #define RSFG_XY2_DECL(N)                                                                                  \
   int xy2_group_##N(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0,   \
                     float2* P1, int z_begin, int z_end, const XYMaps& m, cudaStream_t st);                 \
   int xy2_group_box_##N(int r, int ty, int* bx, int* by);
 RSFG_XY2_GROUPS(RSFG_XY2_DECL)
 #undef RSFG_XY2_DECL
+
+// Body of one radius-group translation unit (rsfg_xy2_g*.cu): the TMA box and
+// the launch of every radius in RADII (64 x 64 tiles: fields=2 only, the
+// fields=4 tile exceeds shared memory).
+#define RSFG_XY2_BOX_CASE(R)                                       \
+  case R:                                                          \
+    *bx = ty == 64 ? XY2<R, 1, 64>::BOXX : XY2<R, 1, 32>::BOXX;    \
+    *by = ty == 64 ? XY2<R, 1, 64>::WY : XY2<R, 1, 32>::WY;        \
+    return 1;
+#define RSFG_XY2_LAUNCH_CASE(R)                                                                       \
+  case R:                                                                                             \
+    if (ty == 64) return fields == 4 ? -1 : xy2_launch<R, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st); \
+    return fields == 4 ? xy2_launch<R, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)                  \
+                       : xy2_launch<R, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
+#define RSFG_XY2_GROUP(N, RADII)                                                                              \
+  int xy2_group_box_##N(int r, int ty, int* bx, int* by) {                                                  \
+    switch (r) {                                                                                            \
+      RADII(RSFG_XY2_BOX_CASE)                                                                              \
+      default:                                                                                              \
+        return -2;                                                                                          \
+    }                                                                                                       \
+  }                                                                                                         \
+  int xy2_group_##N(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0,     \
+                    float2* P1, int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {                 \
+    switch (r) {                                                                                            \
+      RADII(RSFG_XY2_LAUNCH_CASE)                                                                           \
+      default:                                                                                              \
+        return -2;                                                                                          \
+    }                                                                                                       \
+  }
 
 }  // namespace rsfg

@@ -1,58 +1,8 @@
 // rsfg_xy2_g1.cu -- xy2 (rsfg_xy2.cuh) instantiations for radii [5, 6, 7, 8];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_xy2.cuh"
 
 namespace rsfg {
-
-int xy2_group_box_1(int r, int ty, int* bx, int* by) {
-  switch (r) {
-    case 5:
-      *bx = ty == 64 ? XY2<5, 1, 64>::BOXX : XY2<5, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<5, 1, 64>::WY : XY2<5, 1, 32>::WY;
-      return 1;
-    case 6:
-      *bx = ty == 64 ? XY2<6, 1, 64>::BOXX : XY2<6, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<6, 1, 64>::WY : XY2<6, 1, 32>::WY;
-      return 1;
-    case 7:
-      *bx = ty == 64 ? XY2<7, 1, 64>::BOXX : XY2<7, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<7, 1, 64>::WY : XY2<7, 1, 32>::WY;
-      return 1;
-    case 8:
-      *bx = ty == 64 ? XY2<8, 1, 64>::BOXX : XY2<8, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<8, 1, 64>::WY : XY2<8, 1, 32>::WY;
-      return 1;
-    default:
-      return -2;
-  }
-}
-
-int xy2_group_1(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0, float2* P1,
-                 int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 5:
-      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
-        return fields == 4 ? -1 : xy2_launch<5, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<5, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<5, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    case 6:
-      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
-        return fields == 4 ? -1 : xy2_launch<6, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<6, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<6, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    case 7:
-      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
-        return fields == 4 ? -1 : xy2_launch<7, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<7, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<7, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    case 8:
-      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
-        return fields == 4 ? -1 : xy2_launch<8, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<8, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<8, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(5) X(6) X(7) X(8)
+RSFG_XY2_GROUP(1, RADII)
 }  // namespace rsfg

@@ -1,31 +1,8 @@
 // rsfg_xy2_g6.cu -- xy2 (rsfg_xy2.cuh) instantiations for radii [18];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_xy2.cuh"
 
 namespace rsfg {
-
-int xy2_group_box_6(int r, int ty, int* bx, int* by) {
-  switch (r) {
-    case 18:
-      *bx = ty == 64 ? XY2<18, 1, 64>::BOXX : XY2<18, 1, 32>::BOXX;
-      *by = ty == 64 ? XY2<18, 1, 64>::WY : XY2<18, 1, 32>::WY;
-      return 1;
-    default:
-      return -2;
-  }
-}
-
-int xy2_group_6(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0, float2* P1,
-                 int z_begin, int z_end, const XYMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 18:
-      if (ty == 64)  // 64 x 64 tiles: fields=2 only (the fields=4 tile exceeds shared memory)
-        return fields == 4 ? -1 : xy2_launch<18, 1, 64>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-      return fields == 4 ? xy2_launch<18, 2, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st)
-                         : xy2_launch<18, 1, 32>(g, t1, inv_eps, P0, P1, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(18)
+RSFG_XY2_GROUP(6, RADII)
 }  // namespace rsfg

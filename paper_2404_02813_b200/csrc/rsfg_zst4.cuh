@@ -468,12 +468,40 @@ int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuf
 }  // namespace
 
 // Per-radius-group entry points (rsfg_zst4_g*.cu): -2 when r is not in the group.
-#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
 #define RSFG_ZST4_DECL(N)                                                                              \
   int zst4_group_##N(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c,             \
                      const StepBuffers& b, int z_begin, int z_end, const ZMaps& m, cudaStream_t st);    \
   int zst4_group_box_##N(int r, int fields, int* pbox_z, int* ty);
 RSFG_ZST4_GROUPS(RSFG_ZST4_DECL)
 #undef RSFG_ZST4_DECL
+
+// Body of one radius-group translation unit (rsfg_zst4_g*.cu): the P-window
+// box (rows = the launched kernel's tile) and the launch of every radius in RADII.
+#define RSFG_ZST4_BOX_CASE(R)                                                   \
+  case R:                                                                       \
+    *pbox_z = Z4<R, 1>::NW;                                                     \
+    *ty = fields == 4 ? Z4<R, 2>::TY : Z4<R, 1>::TY;                            \
+    return (fields == 4 ? Z4<R, 2>::kSmem : Z4<R, 1>::kSmem) <= 227 * 1024;
+#define RSFG_ZST4_LAUNCH_CASE(R)                                                \
+  case R:                                                                       \
+    return fields == 4 ? zst4_launch<R, 2>(g, t1, c, b, z_begin, z_end, m, st)  \
+                       : zst4_launch<R, 1>(g, t1, c, b, z_begin, z_end, m, st);
+#define RSFG_ZST4_GROUP(N, RADII)                                                                            \
+  int zst4_group_box_##N(int r, int fields, int* pbox_z, int* ty) {                                        \
+    switch (r) {                                                                                           \
+      RADII(RSFG_ZST4_BOX_CASE)                                                                            \
+      default:                                                                                             \
+        return -2;                                                                                         \
+    }                                                                                                      \
+  }                                                                                                        \
+  int zst4_group_##N(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c,                 \
+                     const StepBuffers& b, int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {      \
+    switch (r) {                                                                                           \
+      RADII(RSFG_ZST4_LAUNCH_CASE)                                                                         \
+      default:                                                                                             \
+        return -2;                                                                                         \
+    }                                                                                                      \
+  }
 
 }  // namespace rsfg

@@ -1,36 +1,8 @@
 // rsfg_zst4_g1.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [3, 4];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_zst4.cuh"
 
 namespace rsfg {
-
-int zst4_group_box_1(int r, int fields, int* pbox_z, int* ty) {
-  switch (r) {
-    case 3:
-      *pbox_z = Z4<3, 1>::NW;
-      *ty = fields == 4 ? Z4<3, 2>::TY : Z4<3, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<3, 2>::kSmem : Z4<3, 1>::kSmem) <= 227 * 1024;
-    case 4:
-      *pbox_z = Z4<4, 1>::NW;
-      *ty = fields == 4 ? Z4<4, 2>::TY : Z4<4, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<4, 2>::kSmem : Z4<4, 1>::kSmem) <= 227 * 1024;
-    default:
-      return -2;
-  }
-}
-
-int zst4_group_1(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
-                  int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 3:
-      return fields == 4 ? zst4_launch<3, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<3, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 4:
-      return fields == 4 ? zst4_launch<4, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<4, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(3) X(4)
+RSFG_ZST4_GROUP(1, RADII)
 }  // namespace rsfg

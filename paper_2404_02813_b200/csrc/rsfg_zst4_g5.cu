@@ -1,29 +1,8 @@
 // rsfg_zst4_g5.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [9];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_zst4.cuh"
 
 namespace rsfg {
-
-int zst4_group_box_5(int r, int fields, int* pbox_z, int* ty) {
-  switch (r) {
-    case 9:
-      *pbox_z = Z4<9, 1>::NW;
-      *ty = fields == 4 ? Z4<9, 2>::TY : Z4<9, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<9, 2>::kSmem : Z4<9, 1>::kSmem) <= 227 * 1024;
-    default:
-      return -2;
-  }
-}
-
-int zst4_group_5(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
-                  int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 9:
-      return fields == 4 ? zst4_launch<9, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<9, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(9)
+RSFG_ZST4_GROUP(5, RADII)
 }  // namespace rsfg

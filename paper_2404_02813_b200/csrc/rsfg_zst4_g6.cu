@@ -1,36 +1,8 @@
 // rsfg_zst4_g6.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [10, 11];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_zst4.cuh"
 
 namespace rsfg {
-
-int zst4_group_box_6(int r, int fields, int* pbox_z, int* ty) {
-  switch (r) {
-    case 10:
-      *pbox_z = Z4<10, 1>::NW;
-      *ty = fields == 4 ? Z4<10, 2>::TY : Z4<10, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<10, 2>::kSmem : Z4<10, 1>::kSmem) <= 227 * 1024;
-    case 11:
-      *pbox_z = Z4<11, 1>::NW;
-      *ty = fields == 4 ? Z4<11, 2>::TY : Z4<11, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<11, 2>::kSmem : Z4<11, 1>::kSmem) <= 227 * 1024;
-    default:
-      return -2;
-  }
-}
-
-int zst4_group_6(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
-                  int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 10:
-      return fields == 4 ? zst4_launch<10, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<10, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 11:
-      return fields == 4 ? zst4_launch<11, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<11, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(10) X(11)
+RSFG_ZST4_GROUP(6, RADII)
 }  // namespace rsfg

@@ -1,36 +1,8 @@
 // rsfg_zst4_g7.cu -- zst4 (rsfg_zst4.cuh) instantiations for radii [12, 15];
-// split across translation units so the build parallelises.
+// one translation unit per radius group so the build parallelises.
 #include "rsfg_zst4.cuh"
 
 namespace rsfg {
-
-int zst4_group_box_7(int r, int fields, int* pbox_z, int* ty) {
-  switch (r) {
-    case 12:
-      *pbox_z = Z4<12, 1>::NW;
-      *ty = fields == 4 ? Z4<12, 2>::TY : Z4<12, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<12, 2>::kSmem : Z4<12, 1>::kSmem) <= 227 * 1024;
-    case 15:
-      *pbox_z = Z4<15, 1>::NW;
-      *ty = fields == 4 ? Z4<15, 2>::TY : Z4<15, 1>::TY;  // box rows = the launched kernel's tile
-      return (fields == 4 ? Z4<15, 2>::kSmem : Z4<15, 1>::kSmem) <= 227 * 1024;
-    default:
-      return -2;
-  }
-}
-
-int zst4_group_7(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c, const StepBuffers& b,
-                  int z_begin, int z_end, const ZMaps& m, cudaStream_t st) {
-  switch (r) {
-    case 12:
-      return fields == 4 ? zst4_launch<12, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<12, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    case 15:
-      return fields == 4 ? zst4_launch<15, 2>(g, t1, c, b, z_begin, z_end, m, st)
-                         : zst4_launch<15, 1>(g, t1, c, b, z_begin, z_end, m, st);
-    default:
-      return -2;
-  }
-}
-
+#define RADII(X) X(12) X(15)
+RSFG_ZST4_GROUP(7, RADII)
 }  // namespace rsfg

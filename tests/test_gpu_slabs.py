@@ -85,9 +85,15 @@ def test_evolve_multi_blowup_and_thin():
     import paper_2404_02813_b200 as rsf
     img, phi, _ = case(40, 36, 32)
     bad = np.array(phi)
-    bad[20, 5, 7] = np.nan
-    with pytest.raises(rsf.BlowupError, match=r"voxel \(7,5,20\), iteration 1"):
-        rsf.evolve_multi(bad, img, rsf.RsfParams(sigma1=2.0, max_iters=5), [0, 0])
+    bad[20, 5, 7] = np.nan  # spreads to z = 18 through the normals within the first step
+    p = rsf.RsfParams(sigma1=2.0, max_iters=5)
+    with pytest.raises(rsf.BlowupError) as one:
+        rsf.evolve(bad, img, p)
+    assert "iteration 1" in str(one.value)
+    want = str(one.value).split("] ", 1)[1]
+    with pytest.raises(rsf.BlowupError) as multi:  # same first voxel as one device (global min index)
+        rsf.evolve_multi(bad, img, p, [0, 0])
+    assert str(multi.value).split("] ", 1)[1] == want
     with pytest.raises(rsf.ShapeError):
         rsf.evolve_multi(phi, img, rsf.RsfParams(sigma1=3.0, max_iters=5), [0] * 8)
 
