@@ -343,7 +343,8 @@ void make_xy2_maps(rsfg_slab* s) {
   // shared memory); 64 x 32 (2 CTAs/SM) wins up to R = 12
   // (profiles/r01_xy2_tile_height.txt).  RSFG_XY2_TY=32|64 overrides.
   const char* ty = std::getenv("RSFG_XY2_TY");
-  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 && s->fields == 2 ? 64 : 32);
+  // (R >= 19: the 64 x 64 tile's haloed pairs exceed shared memory; 64 x 32)
+  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 && s->t1.r <= 18 && s->fields == 2 ? 64 : 32);
   int bx = 0, by = 0;
   if (!rsfg::xy2_box(s->t1.r, s->xy2_ty, &bx, &by)) return;
   const int planes = s->ze - s->zb;
@@ -414,7 +415,15 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   std::memset(&s->tid, 0, sizeof s->tid);
   s->tid.w[0] = 1.0f;
   s->tid.r = 0;
-  s->fast = rsfg::has_fast_radius(s->t1.r);
+  // fast path: specialised kernels for this radius that fit shared memory
+  // (kernel 1: xy2 when rows are 16-byte aligned, else the LDG-staged xy)
+  {
+    const int r = s->t1.r;
+    const int ty = (r >= 15 && r <= 18 && s->fields == 2) ? 64 : 32;
+    s->fast = rsfg::has_fast_radius(r) &&
+              (((nx % 4) == 0 && (rsfg::xy2_fits(r, s->fields, ty) || rsfg::xy2_fits(r, s->fields, 32))) ||
+               rsfg::xy_fits(r, s->fields));
+  }
   s->env_key = variant_env_key();
   s->nx = nx;
   s->ny = ny;
@@ -458,6 +467,8 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   if (s->fields == 4) CUDA_TRY(cudaMalloc(&s->P[1], held * sizeof(float2)));
   if (!s->fast) CUDA_TRY(cudaMalloc(&s->scratch, held * sizeof(float2) * (s->fields == 4 ? 4 : 2)));
   CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
+  // the whole ring is read back at each check (only the stepped slots matter)
+  CUDA_TRY(cudaMemsetAsync(s->counters, 0, kSlots * 2 * sizeof(unsigned long long), s->stream));
   CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&s->flags, 2 * sizeof(unsigned int)));

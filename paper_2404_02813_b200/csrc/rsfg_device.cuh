@@ -7,10 +7,11 @@
 
 #include "rsfg_internal.h"
 
-// Radii with a specialised (register-window) kernel -- every sigma <= 6 (R = ceil(3 sigma) <= 18);
-// larger radii take the generic path.
-#define RSFG_RADII(X) \
-  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)
+// Radii with a specialised (register-window) kernel -- every sigma <= 8 (R = ceil(3 sigma) <= 24);
+// larger radii take the generic runtime-tap path.
+#define RSFG_RADII(X)                                                                                  \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18) \
+  X(19) X(20) X(21) X(22) X(23) X(24)
 
 namespace rsfg {
 namespace {

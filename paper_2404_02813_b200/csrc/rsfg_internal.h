@@ -58,6 +58,10 @@ enum StepMode { kUpdate = 0, kEnergy = 1 };
 
 // True when a fused, radius-specialised kernel exists for r.
 bool has_fast_radius(int r);
+// Whether kernel 1's specialised variants fit shared memory for (r, fields):
+// xy2 with tile height ty (TMA, nx % 4 == 0) and the LDG-staged xy.
+bool xy2_fits(int r, int fields, int ty);
+bool xy_fits(int r, int fields);
 
 // TMA descriptors of kernel 1's input tiles (3-D fp32 maps of the held
 // planes, box = xy_tma_box(R)).  valid == false -> LDG loads.

@@ -21,7 +21,15 @@ namespace {
 
 constexpr size_t kChunk = 16u << 20;  // bytes per pinned chunk
 constexpr int kRing = 4;              // chunks in flight
-constexpr int kThreads = 8;           // host threads per chunk memcpy
+constexpr int kMaxThreads = 16;       // host threads per chunk memcpy (cap)
+
+int copy_threads() {
+  static const int n = [] {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return (int)std::min<unsigned>(kMaxThreads, std::max(1u, hw / 2));
+  }();
+  return n;
+}
 
 struct Pool {
   std::mutex mu;
@@ -50,18 +58,19 @@ bool pool_ready(Pool& p) {
 }
 
 void par_memcpy(void* dst, const void* src, size_t n) {
-  const size_t per = (n + kThreads - 1) / kThreads;
-  if (n < (1u << 20)) {
+  const int nt = copy_threads();
+  const size_t per = (n + nt - 1) / nt;
+  if (n < (1u << 20) || nt == 1) {
     std::memcpy(dst, src, n);
     return;
   }
-  std::thread th[kThreads - 1];
-  for (int t = 1; t < kThreads; ++t) {
+  std::thread th[kMaxThreads - 1];
+  for (int t = 1; t < nt; ++t) {
     const size_t a = std::min(n, t * per), b = std::min(n, a + per);
     th[t - 1] = std::thread([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
   }
   std::memcpy(dst, src, std::min(n, per));
-  for (auto& t : th) t.join();
+  for (int t = 1; t < nt; ++t) th[t - 1].join();
 }
 
 }  // namespace

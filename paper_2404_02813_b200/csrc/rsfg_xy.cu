@@ -159,6 +159,9 @@ template <int R, int NP, bool TMA>
 int xy_launch(const Geom& g, const Taps& t, float inv_eps, const float* phi, const float* image, float2* P0,
               float2* P1, int z_begin, int z_end, const XYMaps* maps, cudaStream_t st) {
   using C = XYCfg<R, NP, kXYTX, kXYTY, kBX, kBY>;
+  if constexpr (C::kSmem > 227 * 1024) {
+    return -1;  // setup routes such (radius, fields) to the generic path (xy_fits)
+  } else {
   auto k = xy_kernel<R, NP, kXYTX, kXYTY, kBX, kBY, TMA>;
   smem_optin<xy_kernel<R, NP, kXYTX, kXYTY, kBX, kBY, TMA>>((int)C::kSmem);
   if (z_end <= z_begin) return 0;
@@ -168,6 +171,7 @@ int xy_launch(const Geom& g, const Taps& t, float inv_eps, const float* phi, con
   dim3 grid((g.nx + kXYTX - 1) / kXYTX, (g.ny + kXYTY - 1) / kXYTY, z_end - z_begin);
   k<<<grid, C::kThreads, C::kSmem, st>>>(g, t, inv_eps, phi, image, P0, P1, z_begin, mp, mi);
   return 1;
+  }
 }
 
 template <int R, int NP>
@@ -179,6 +183,19 @@ int xy_dispatch(const Geom& g, const Taps& t, float inv_eps, const float* phi, c
 }
 
 }  // namespace
+
+bool xy_fits(int r, int fields) {
+  switch (r) {
+#define CASE(R)                                                                                        \
+  case R:                                                                                              \
+    return (fields == 4 ? XYCfg<R, 2, kXYTX, kXYTY, kBX, kBY>::kSmem : XYCfg<R, 1, kXYTX, kXYTY, kBX, kBY>::kSmem) <= \
+           227 * 1024;
+    RSFG_RADII(CASE)
+#undef CASE
+    default:
+      return false;
+  }
+}
 
 bool xy_tma_box(int r, int* bx, int* by) {
   switch (r) {

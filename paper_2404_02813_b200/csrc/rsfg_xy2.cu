@@ -4,6 +4,21 @@
 
 namespace rsfg {
 
+// Whether xy2's kernel for (r, fields, ty) fits shared memory (setup uses it
+// to pick the fast path; large radii with fields=4 can exceed 227 KB).
+bool xy2_fits(int r, int fields, int ty) {
+  switch (r) {
+#define CASE(R)                                                                                     \
+  case R:                                                                                           \
+    if (ty == 64) return fields == 2 && R <= 18 && XY2<R, 1, 64>::kSmem <= 227 * 1024;              \
+    return (fields == 4 ? XY2<R, 2, 32>::kSmem : XY2<R, 1, 32>::kSmem) <= 227 * 1024;
+    RSFG_RADII(CASE)
+#undef CASE
+    default:
+      return false;
+  }
+}
+
 bool xy2_box(int r, int ty, int* bx, int* by) {
   int rc = -2;
 #define TRY(N) \

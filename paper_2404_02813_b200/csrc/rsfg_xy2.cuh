@@ -62,6 +62,19 @@ struct XY2 {
   static constexpr int YIT = (NP * WX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
   static constexpr int XIT = (NP * TY * (TX / BX) + NT - 1) / NT;  // x-pass items per thread
   static constexpr int OIT = (NP * TY * TX / 2 + NT - 1) / NT;     // copy-out float4 per thread
+  // Stored-Heaviside variant's y pass: the WX window columns x NSEGH row
+  // segments of BYH outputs, sized so the items fill the CTA once (64 x 32,
+  // R = 9: 82 x 3 = 246 items of 11 rows, where 8-row segments gave 328 items
+  // = 1.28 rounds with 72 threads busy in the second).  The last segment ends
+  // at row TY and may overlap its neighbour (same values written twice).
+  static constexpr int nsegh() {
+    int s = NT / WX > 0 ? NT / WX : 1;
+    while ((TY + s - 1) / s > 12) ++s;
+    return s;
+  }
+  static constexpr int NSEGH = nsegh();
+  static constexpr int BYH = (TY + NSEGH - 1) / NSEGH;
+  static constexpr int YITH = (WX * NSEGH + NT - 1) / NT;
 };
 
 template <int R, int NP, int TY, bool EDGE>
@@ -295,16 +308,17 @@ __device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, floa
   const int tid = threadIdx.x;
   const int bx0 = x0 - R - C::SHIFT, by0 = y0 - R;
 
-  int ysrc[C::YIT], ydst[C::YIT];
-  constexpr int SEGY = TY / C::BY;
+  int ysrc[C::YITH], ydst[C::YITH], yskip[C::YITH];
 #pragma unroll
-  for (int i = 0; i < C::YIT; ++i) {
-    const int it = min(tid + i * C::NT, C::WX * SEGY - 1);
+  for (int i = 0; i < C::YITH; ++i) {
+    const int it = min(tid + i * C::NT, C::WX * C::NSEGH - 1);
     const int sy = it / C::WX, cx = it - sy * C::WX;
-    ysrc[i] = (sy * C::BY) * C::BOXX + C::SHIFT + cx;
-    ydst[i] = (sy * C::BY) * C::PY + cx;
+    const int r0 = sy < C::NSEGH - 1 ? sy * C::BYH : TY - C::BYH;
+    ysrc[i] = r0 * C::BOXX + C::SHIFT + cx;
+    ydst[i] = r0 * C::PY + cx;
+    yskip[i] = sy < C::NSEGH - 1 ? 0 : (C::NSEGH - 1) * C::BYH - r0;  // rows the previous segment wrote
   }
-  const bool y_last = tid + (C::YIT - 1) * C::NT < C::WX * SEGY;
+  const bool y_last = tid + (C::YITH - 1) * C::NT < C::WX * C::NSEGH;
   int xsrc[C::XIT], xdst[C::XIT];
   constexpr int SEGX = C::TX / C::BX;
 #pragma unroll
@@ -370,19 +384,19 @@ __device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, floa
     }
     // ---- y pass straight from the tile (lanes walk x: consecutive pairs)
 #pragma unroll
-    for (int i = 0; i < C::YIT; ++i) {
-      if (i < C::YIT - 1 || y_last) {
+    for (int i = 0; i < C::YITH; ++i) {
+      if (i < C::YITH - 1 || y_last) {
         const float2* src = T + ysrc[i];
-        float2 v[C::BY + 2 * R];
+        float2 v[C::BYH + 2 * R];
 #pragma unroll
-        for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::BOXX];
+        for (int k = 0; k < C::BYH + 2 * R; ++k) v[k] = src[k * C::BOXX];
         float2* dst = Ys + ydst[i];
 #pragma unroll
-        for (int b = 0; b < C::BY; ++b) {
+        for (int b = 0; b < C::BYH; ++b) {
           float2 acc = fmul2(taps.w[0], v[b]);
 #pragma unroll
           for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-          dst[b * C::PY] = acc;
+          if (b >= yskip[i]) dst[b * C::PY] = acc;
         }
       }
     }
@@ -456,7 +470,7 @@ template <int R, int TY>
 int xy2_hh_launch(const Geom& g, const Taps& t, float2* P0, int z_begin, int z_end, const XYMaps& m,
                   cudaStream_t st) {
   using C = XY2<R, 1, TY>;
-  if (C::kSmemHH > 227 * 1024) return -1;
+  static_assert(C::kSmemHH <= 227 * 1024, "stored-Heaviside tile exceeds shared memory");
   auto k = xy2_hh_kernel<R, TY>;
   if (!smem_optin<xy2_hh_kernel<R, TY>>((int)C::kSmemHH)) return -1;
   if (z_end <= z_begin) return 0;
@@ -475,13 +489,18 @@ int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* 
   }
   if (m.use_hh && NP == 1) return -1;
   using C = XY2<R, NP, TY>;
-  if (C::kSmem > 227 * 1024) return -1;
-  auto k = xy2_kernel<R, NP, TY>;
-  if (!smem_optin<xy2_kernel<R, NP, TY>>((int)C::kSmem)) return -1;
-  if (z_end <= z_begin) return 0;
-  dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
-  k<<<grid, C::NT, C::kSmem, st>>>(g, t, inv_eps, P0, P1, z_begin, z_end, m.phi, m.img);
-  return 1;
+  // variants that cannot fit shared memory (or that setup never selects:
+  // 64-row tiles past R = 18) are not instantiated
+  if constexpr (C::kSmem > 227 * 1024 || (TY == 64 && R > 18)) {
+    return -1;
+  } else {
+    auto k = xy2_kernel<R, NP, TY>;
+    if (!smem_optin<xy2_kernel<R, NP, TY>>((int)C::kSmem)) return -1;
+    if (z_end <= z_begin) return 0;
+    dim3 grid((g.nx + C::TX - 1) / C::TX, (g.ny + TY - 1) / TY, (z_end - z_begin + C::NZC - 1) / C::NZC);
+    k<<<grid, C::NT, C::kSmem, st>>>(g, t, inv_eps, P0, P1, z_begin, z_end, m.phi, m.img);
+    return 1;
+  }
 }
 
 }  // namespace
@@ -489,7 +508,7 @@ int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* 
 // kernel 1 tile height used by xy2 (RSFG_XY2_TY overrides: 32 or 64)
 constexpr int kXY2DefaultTY = 32;
 
-#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+#define RSFG_XY2_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11)
 #define RSFG_XY2_DECL(N)                                                                                  \
   int xy2_group_##N(int r, int ty, const Geom& g, int fields, const Taps& t1, float inv_eps, float2* P0,   \
                     float2* P1, int z_begin, int z_end, const XYMaps& m, cudaStream_t st);                 \

@@ -299,7 +299,7 @@ template <int R, int NP>
 int zst_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuffers& b, int z_begin,
                int z_end, int mode, cudaStream_t st) {
   // z-pass register window = TZC + 2R float2: halve the chunk for large radii
-  constexpr int TZC = R > 12 ? kZTZC / 2 : kZTZC;
+  constexpr int TZC = R > 18 ? kZTZC / 4 : (R > 12 ? kZTZC / 2 : kZTZC);
   constexpr int NCH = kZTZC * kZNCH / TZC;
   using C = ZCfg<R, NP, kZTX, kZTY, TZC, NCH>;
   auto k = zst_kernel<R, NP, kZTX, kZTY, TZC, NCH>;

@@ -44,7 +44,6 @@ struct Z4 {
   // 32 x 8 columns; 32 x 4 for large radii, whose z-pass window (8 + 2R
   // planes of P) would otherwise leave one CTA per SM.
   static constexpr int TX = 32, TY = R >= 17 ? 4 : (R <= 9 && NP == 1 ? kZ4TallTY : 8), NT = TX * TY;
-  static constexpr int kMinBlocks = TY == 16 ? 1 : (TY == 4 && NP == 1 ? 3 : 2);  // CTAs per SM for the registers
   static constexpr int BX = 40, BY = TY + 4, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
@@ -60,6 +59,10 @@ struct Z4 {
   static constexpr size_t kKBytes = (size_t)8 * NK * NT * sizeof(float);
   static constexpr size_t kNrBytes = (size_t)2 * 2 * NPL * sizeof(float);
   static constexpr size_t kSmem = kPBytes + kPhiBytes + kKBytes + kNrBytes + 16 * sizeof(uint64_t);
+  // CTAs per SM the register budget is sized for: three 32 x 4 CTAs where their
+  // shared memory allows it (R 17-18), else two (one for 32 x 16 tiles)
+  static constexpr int kMinBlocks =
+      TY == 16 ? 1 : (TY == 4 && NP == 1 && 3 * (kSmem + 1024) <= 228 * 1024 ? 3 : 2);
   static constexpr uint32_t kSlotTx = (uint32_t)((SLOT + NK * NT) * sizeof(float));
 };
 
@@ -468,7 +471,7 @@ int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuf
 }  // namespace
 
 // Per-radius-group entry points (rsfg_zst4_g*.cu): -2 when r is not in the group.
-#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
+#define RSFG_ZST4_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13)
 #define RSFG_ZST4_DECL(N)                                                                              \
   int zst4_group_##N(int r, const Geom& g, int fields, const Taps& t1, const StepConsts& c,             \
                      const StepBuffers& b, int z_begin, int z_end, const ZMaps& m, cudaStream_t st);    \
