@@ -530,7 +530,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="weak", choices=["weak", *STRONG])
     ap.add_argument("--fields", type=int, default=2, choices=[2, 4])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl", "host"], help="N > 1 halo transport")

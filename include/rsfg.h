@@ -98,6 +98,7 @@ typedef struct rsfg_report {
   double ms_h2d, ms_init, ms_loop, ms_d2h; /* CUDA-event timings of the call's phases    */
   int64_t gpu_launches;           /* kernels launched by the call                     */
   double stage_seconds[RSFG_STAGE_COUNT]; /* options.profile_stages: per-row kernel time */
+  double ms_setup;                /* rsfg_evolve: host time to allocate/configure the workspace */
 } rsfg_report;
 
 /* Called every stop_every iterations with the current phi (host copy);

@@ -69,6 +69,7 @@ class rsfg_report(C.Structure):
         ("ms_d2h", C.c_double),
         ("gpu_launches", C.c_int64),
         ("stage_seconds", C.c_double * RSFG_STAGE_COUNT),
+        ("ms_setup", C.c_double),
     ]
 
 

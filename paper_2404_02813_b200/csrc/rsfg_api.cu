@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -124,7 +125,7 @@ struct rsfg_slab {
   float2* P[2] = {nullptr, nullptr};
   float2* scratch = nullptr;
   unsigned long long* counters = nullptr;   // device [kSlots][2]
-  unsigned long long* h_counters = nullptr; // pinned mirror
+  unsigned long long* h_counters = nullptr; // host mirror (ordinary memory: 1 KB, read after a sync)
   unsigned int* mm = nullptr;               // device min/max scratch
   rsfg::XYMaps xymaps[2] = {};              // TMA maps for kernel 1, per phi buffer
   rsfg::ZMaps zmaps[2] = {};                // TMA maps for kernel 2 (zst4), per phi buffer
@@ -141,6 +142,10 @@ struct rsfg_slab {
   // kernel launch of a step is bracketed by a CUDA-event pair tagged with the
   // reference stage row that carries its time (kStage* below).
   bool prof_on = false;
+  // rsfg_evolve workspaces come from the library's stream-ordered pool (freed
+  // memory stays cached for the next call up to a threshold; slabs, whose
+  // buffers may be exported over CUDA IPC, use plain cudaMalloc)
+  bool pooled = false;
   std::vector<cudaEvent_t> prof_ev;  // 2 per launch group
   std::vector<int> prof_stage;
   int prof_used = 0;
@@ -213,21 +218,66 @@ std::string variant_env_key() {
 
 namespace {
 
+// Per-device stream-ordered memory pool for rsfg_evolve's workspace.  A
+// workspace returned to it stays mapped (up to 1/8 of the device memory) so a
+// repeated call skips cudaMalloc/cudaFree of several GB -- which measured
+// 4 ms to 0.6 s per call on B200 (profiles/r02_e2e_probe.jsonl).
+// rsfg_release_workspace() trims it.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t lib_pool(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&g_pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      g_pools[dev] = nullptr;
+      return nullptr;
+    }
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t keep = total_b / 8;
+    cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return g_pools[dev];
+}
+
+cudaError_t dev_alloc(rsfg_slab* s, void** p, size_t bytes) {
+  if (s->pooled) {
+    if (cudaMemPool_t pool = lib_pool(s->dev)) return cudaMallocFromPoolAsync(p, bytes, pool, s->stream);
+  }
+  return cudaMalloc(p, bytes);
+}
+
+void dev_free(rsfg_slab* s, void* p) {
+  if (!p) return;
+  if (s->pooled)
+    cudaFreeAsync(p, s->stream);
+  else
+    cudaFree(p);
+}
+
 void release(rsfg_slab* s) {
   if (!s) return;
   cudaSetDevice(s->dev);
-  cudaFree(s->phi[0]);
-  cudaFree(s->phi[1]);
-  cudaFree(s->image);
-  cudaFree(s->k1i);
-  if (s->ki != s->image) cudaFree(s->ki);
-  cudaFree(s->P[0]);
-  cudaFree(s->P[1]);
-  cudaFree(s->scratch);
-  cudaFree(s->hh);
-  cudaFree(s->counters);
-  cudaFree(s->mm);
-  if (s->h_counters) cudaFreeHost(s->h_counters);
+  dev_free(s, s->phi[0]);
+  dev_free(s, s->phi[1]);
+  dev_free(s, s->image);
+  dev_free(s, s->k1i);
+  if (s->ki != s->image) dev_free(s, s->ki);
+  dev_free(s, s->P[0]);
+  dev_free(s, s->P[1]);
+  dev_free(s, s->scratch);
+  dev_free(s, s->hh);
+  dev_free(s, s->counters);
+  dev_free(s, s->mm);
+  delete[] s->h_counters;
+  s->h_counters = nullptr;
   for (cudaEvent_t e : s->prof_ev) cudaEventDestroy(e);
   s->prof_ev.clear();
   if (s->push_stream) cudaStreamSynchronize(s->push_stream), cudaStreamDestroy(s->push_stream);
@@ -236,7 +286,7 @@ void release(rsfg_slab* s) {
   for (auto& L : s->link)
     for (void* b : L.ipc_base)
       if (b) cudaIpcCloseMemHandle(b);
-  cudaFree(s->flags);
+  dev_free(s, s->flags);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -455,26 +505,27 @@ int setup(rsfg_slab* s, int nx, int ny, int nz, int z0, int z1, const rsfg_param
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->own_stream = true;
   const size_t held = s->held();
-  CUDA_TRY(cudaMalloc(&s->phi[0], held * sizeof(float)));
-  CUDA_TRY(cudaMalloc(&s->phi[1], held * sizeof(float)));
-  CUDA_TRY(cudaMalloc(&s->image, held * sizeof(float)));
-  if (s->fields == 2) CUDA_TRY(cudaMalloc(&s->k1i, held * sizeof(float)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->phi[0], held * sizeof(float)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->phi[1], held * sizeof(float)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->image, held * sizeof(float)));
+  if (s->fields == 2) CUDA_TRY(dev_alloc(s, (void**)&s->k1i, held * sizeof(float)));
   if (s->t2.r > 0)
-    CUDA_TRY(cudaMalloc(&s->ki, held * sizeof(float)));
+    CUDA_TRY(dev_alloc(s, (void**)&s->ki, held * sizeof(float)));
   else
     s->ki = s->image;
-  CUDA_TRY(cudaMalloc(&s->P[0], held * sizeof(float2)));
-  if (s->fields == 4) CUDA_TRY(cudaMalloc(&s->P[1], held * sizeof(float2)));
-  if (!s->fast) CUDA_TRY(cudaMalloc(&s->scratch, held * sizeof(float2) * (s->fields == 4 ? 4 : 2)));
-  CUDA_TRY(cudaMalloc(&s->counters, kSlots * 2 * sizeof(unsigned long long)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->P[0], held * sizeof(float2)));
+  if (s->fields == 4) CUDA_TRY(dev_alloc(s, (void**)&s->P[1], held * sizeof(float2)));
+  if (!s->fast) CUDA_TRY(dev_alloc(s, (void**)&s->scratch, held * sizeof(float2) * (s->fields == 4 ? 4 : 2)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->counters, kSlots * 2 * sizeof(unsigned long long)));
   // the whole ring is read back at each check (only the stepped slots matter)
   CUDA_TRY(cudaMemsetAsync(s->counters, 0, kSlots * 2 * sizeof(unsigned long long), s->stream));
-  CUDA_TRY(cudaMalloc(&s->mm, 2 * sizeof(unsigned int)));
-  CUDA_TRY(cudaMallocHost(&s->h_counters, kSlots * 2 * sizeof(unsigned long long)));
-  CUDA_TRY(cudaMalloc(&s->flags, 2 * sizeof(unsigned int)));
+  CUDA_TRY(dev_alloc(s, (void**)&s->mm, 2 * sizeof(unsigned int)));
+  // (not cudaMallocHost: page-locking per call stalls when much memory is pinned)
+  s->h_counters = new unsigned long long[kSlots * 2]();
+  CUDA_TRY(dev_alloc(s, (void**)&s->flags, 2 * sizeof(unsigned int)));
   CUDA_TRY(cudaMemsetAsync(s->flags, 0, 2 * sizeof(unsigned int), s->stream));
   if (s->fast && s->fields == 2 && s->t2.r == 0 && (s->nx % 4) == 0)
-    CUDA_TRY(cudaMalloc(&s->hh, held * sizeof(float2)));
+    CUDA_TRY(dev_alloc(s, (void**)&s->hh, held * sizeof(float2)));
   make_xy_maps(s);
   make_z_maps(s);
   make_xy2_maps(s);
@@ -1047,14 +1098,17 @@ int evolve_impl(const float* image, float* phi, int nx, int ny, int nz, const rs
       t_cache.st = nullptr;
     }
   }
+  const auto t_setup = std::chrono::steady_clock::now();
   if (!st) {
     st = new rsfg_state;
+    st->e.pooled = true;
     if (int rc = setup(&st->e, nx, ny, nz, 0, nz, p, &opt)) {
       release(&st->e);
       delete st;
       return rc;
     }
   }
+  rep->ms_setup = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count();
   rsfg_slab* s = &st->e;
   struct StGuard {
     rsfg_state* st;
@@ -1193,6 +1247,9 @@ __attribute__((visibility("default"))) int rsfg_evolve(const float* image, float
 __attribute__((visibility("default"))) void rsfg_release_workspace(void) {
   rsfg_state_destroy(t_cache.st);
   t_cache.st = nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t p : g_pools)
+    if (p) cudaMemPoolTrimTo(p, 0);  // cached workspace memory back to the device
 }
 
 __attribute__((visibility("default"))) int rsfg_extract_mask(const float* phi, float* mask, int64_t n, int32_t device) {

@@ -66,15 +66,34 @@ struct XY2 {
   // segments of BYH outputs, sized so the items fill the CTA once (64 x 32,
   // R = 9: 82 x 3 = 246 items of 11 rows, where 8-row segments gave 328 items
   // = 1.28 rounds with 72 threads busy in the second).  The last segment ends
-  // at row TY and may overlap its neighbour (same values written twice).
-  static constexpr int nsegh() {
-    int s = NT / WX > 0 ? NT / WX : 1;
-    while ((TY + s - 1) / s > 12) ++s;
-    return s;
+  // at row TY and may overlap its neighbour; it skips the rows already stored.
+  // Segment count for np field pairs: least work on the busiest thread
+  // (rounds x (FFMA2 + 2 x LDS.64 per item); shared loads weigh double, the
+  // pass is LSU-heavy), register window BY + 2R <= 52 pairs unless the plain
+  // 8-row split (always a candidate) is already wider.
+  static constexpr long seg_cost(int np, int s) {
+    const int by = (TY + s - 1) / s;
+    return (long)((np * WX * s + NT - 1) / NT) * (by * (2 * R + 1) + 2 * (by + 2 * R));
   }
-  static constexpr int NSEGH = nsegh();
+  static constexpr int nseg(int np) {
+    int best = TY / BY;
+    long best_cost = seg_cost(np, best);
+    for (int s = 1; s <= TY; ++s) {
+      const int by = (TY + s - 1) / s;
+      if (by + 2 * R > 52) continue;
+      if (seg_cost(np, s) < best_cost) best_cost = seg_cost(np, s), best = s;
+    }
+    return best;
+  }
+  static constexpr int NSEGH = nseg(1);
   static constexpr int BYH = (TY + NSEGH - 1) / NSEGH;
   static constexpr int YITH = (WX * NSEGH + NT - 1) / NT;
+  // The Heaviside-computing variant keeps 8-row segments: the cost model's
+  // picks for it (R = 12: 8 x 4 rows; R >= 15: 5 x 13 rows) measured slower or
+  // equal (sigma 4: 1.87 vs 1.81 ms/step) -- its Hs tile traffic dominates.
+  static constexpr int NSEG = TY / BY;
+  static constexpr int BYS = (TY + NSEG - 1) / NSEG;
+  static constexpr int YITS = (NP * WX * NSEG + NT - 1) / NT;
 };
 
 template <int R, int NP, int TY, bool EDGE>
@@ -108,20 +127,22 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
   const bool a_last = a_rg + (C::RITER - 1) * C::RG < C::WY;
   const float* Ta = Tphi + a_rg * C::BOXX + C::C0 + 2 * a_pc;
   float2* Ha = Hs + a_rg * C::PH + C::C0 + 2 * a_pc;
-  // phase B (y pass) items tid + i*NT -> (np, sy, cx): column cx of the window,
-  // outputs sy*BY .. sy*BY+7; lanes walk cx.
-  int ysrc[C::YIT], ydst[C::YIT];
-  constexpr int SEGY = TY / C::BY;
+  // phase B (y pass): lanes walk the window columns cx;
+  // y-pass items (np, segment, column): NSEG row segments of BYS outputs, the
+  // last ending at row TY (rows its neighbour wrote are not stored twice)
+  int ysrc[C::YITS], ydst[C::YITS], yskip[C::YITS];
 #pragma unroll
-  for (int i = 0; i < C::YIT; ++i) {
-    const int it = min(tid + i * C::NT, NP * C::WX * SEGY - 1);
-    const int np = it / (C::WX * SEGY);
-    const int rem = it - np * C::WX * SEGY;
+  for (int i = 0; i < C::YITS; ++i) {
+    const int it = min(tid + i * C::NT, NP * C::WX * C::NSEG - 1);
+    const int np = it / (C::WX * C::NSEG);
+    const int rem = it - np * C::WX * C::NSEG;
     const int sy = rem / C::WX, cx = rem - sy * C::WX;
-    ysrc[i] = np * C::WY * C::PH + (sy * C::BY) * C::PH + C::SHIFT + cx;
-    ydst[i] = np * TY * C::PY + (sy * C::BY) * C::PY + cx;
+    const int r0 = sy < C::NSEG - 1 ? sy * C::BYS : TY - C::BYS;
+    ysrc[i] = np * C::WY * C::PH + r0 * C::PH + C::SHIFT + cx;
+    ydst[i] = np * TY * C::PY + r0 * C::PY + cx;
+    yskip[i] = sy < C::NSEG - 1 ? 0 : (C::NSEG - 1) * C::BYS - r0;
   }
-  const bool y_last = tid + (C::YIT - 1) * C::NT < NP * C::WX * SEGY;
+  const bool y_last = tid + (C::YITS - 1) * C::NT < NP * C::WX * C::NSEG;
   // phase C (x pass) items -> (np, sx, row): lanes walk rows
   int xsrc[C::XIT], xdst[C::XIT];
   constexpr int SEGX = C::TX / C::BX;
@@ -229,19 +250,19 @@ __device__ __forceinline__ void xy2_cta(const Geom& g, const Taps& taps, float i
     // ---- Phase B: y pass on the WX window columns (the first pass carries the
     // x halo: WX/TX < WY/TY).  BY outputs down a column, lanes walk x.
 #pragma unroll
-    for (int i = 0; i < C::YIT; ++i) {
-      if (i < C::YIT - 1 || y_last) {
+    for (int i = 0; i < C::YITS; ++i) {
+      if (i < C::YITS - 1 || y_last) {
         const float2* src = Hs + ysrc[i];
-        float2 v[C::BY + 2 * R];
+        float2 v[C::BYS + 2 * R];
 #pragma unroll
-        for (int k = 0; k < C::BY + 2 * R; ++k) v[k] = src[k * C::PH];
+        for (int k = 0; k < C::BYS + 2 * R; ++k) v[k] = src[k * C::PH];
         float2* dst = Ys + ydst[i];
 #pragma unroll
-        for (int b = 0; b < C::BY; ++b) {
+        for (int b = 0; b < C::BYS; ++b) {
           float2 acc = fmul2(taps.w[0], v[b]);
 #pragma unroll
           for (int j = 1; j <= 2 * R; ++j) acc = ffma2(taps.w[j], v[b + j], acc);
-          dst[b * C::PY] = acc;
+          if (b >= yskip[i]) dst[b * C::PY] = acc;
         }
       }
     }

@@ -38,7 +38,8 @@ def main():
             ph_ms = rep.ms_h2d + rep.ms_init + rep.ms_loop + rep.ms_d2h
             print(json.dumps({"round": rnd, "kind": kind, "wall_ms": round(wall, 1), "h2d": round(rep.ms_h2d, 1),
                               "init": round(rep.ms_init, 1), "loop": round(rep.ms_loop, 1),
-                              "d2h": round(rep.ms_d2h, 1), "outside_ms": round(wall - ph_ms, 1),
+                              "d2h": round(rep.ms_d2h, 1), "setup": round(rep.ms_setup, 1),
+                              "outside_ms": round(wall - ph_ms, 1),
                               "voxel_iter_per_s": n ** 3 * 200 / (wall * 1e-3)}), flush=True)
 
 
