@@ -123,7 +123,12 @@ int rsfg_evolve(const float* image, float* phi_inout, int32_t nx, int32_t ny, in
                 const rsfg_params* p, const rsfg_options* o, rsfg_stop_fn stop, void* user,
                 int32_t stop_every, rsfg_report* report);
 
-/* Frees the calling thread's cached rsfg_evolve workspace (if any). */
+/* rsfg_evolve allocates its device workspace (~32 B/voxel) from the library's
+ * stream-ordered memory pool: after the call the memory stays cached in the
+ * pool, up to 1/8 of the device's memory, so the next call skips cudaMalloc /
+ * cudaFree of several GB (it is NOT held by any state and any later rsfg_evolve
+ * reuses it).  rsfg_release_workspace() frees the calling thread's kept
+ * workspace (options.reuse_workspace) and trims the pools back to the device. */
 void rsfg_release_workspace(void);
 
 /* rsf::extract_mask (rsf.cpp:386-396): mask = phi < 0 ? 1 : 0, on the GPU. */
