@@ -50,7 +50,19 @@ __device__ __forceinline__ float2 ffma2(float w, float2 v, float2 acc) {
   return d;
 }
 
-__device__ __forceinline__ float2 fmul2(float w, float2 v) { return make_float2(w * v.x, w * v.y); }
+// Packed two-lane FP32 multiply (sm_100 FMUL2): w * v on both lanes; the
+// first tap of every pass (same bits as two scalar FMULs, half the issues).
+__device__ __forceinline__ float2 fmul2(float w, float2 v) {
+  float2 d;
+  asm("{\n\t.reg .b64 wv, vv, dv;\n\t"
+      "mov.b64 wv, {%2, %2};\n\t"
+      "mov.b64 vv, {%3, %4};\n\t"
+      "mul.rn.f32x2 dv, wv, vv;\n\t"
+      "mov.b64 {%0, %1}, dv;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(w), "f"(v.x), "f"(v.y));
+  return d;
+}
 
 // atan(q)/pi for q in [0, 1]: q * P(q^2), degree-8 fit; max relative error
 // 1.9e-7 in fp32 (CUDA's atanf is 2 ulp); 9 FMAs, no branches.

@@ -366,3 +366,4 @@ def test_evolve_stop_callback(rsf):
             assert np.array_equal(seen[0][1], st.phi)
     assert np.array_equal(seen[1][1], st.phi)
     assert np.array_equal(got, st.phi)
+
