@@ -187,6 +187,22 @@ inline Volume evolve(Volume phi0, const Volume& I, const RsfParams& p, StopCheck
   return phi0;
 }
 
+// rsf::evolve over several GPUs of this process (rsfg_evolve_multi): z-slabs
+// on `devices` with their halos pushed over NVLink peer memory every step;
+// bitwise equal to evolve() on one GPU.  (No StopCheck: it runs max_iters
+// steps or stops on convergence_fraction.)
+inline Volume evolve_multi(Volume phi0, const Volume& I, const RsfParams& p, const std::vector<int>& devices,
+                           const rsfg_options* options = nullptr) {
+  p.validate();
+  check_same_dims(phi0, I, "evolve");
+  if (devices.empty()) throw param_error("evolve_multi: no devices");
+  const rsfg_params cp = p.c();
+  std::vector<int32_t> dv(devices.begin(), devices.end());
+  check(rsfg_evolve_multi(I.data.data(), phi0.data.data(), I.dims.nx, I.dims.ny, I.dims.nz, &cp, options, dv.data(),
+                          (int32_t)dv.size(), nullptr));
+  return phi0;
+}
+
 // rsf::extract_mask (rsf.hpp:101).
 inline Volume extract_mask(const Volume& phi, int device = 0) {
   Volume m(phi.dims.nx, phi.dims.ny, phi.dims.nz);

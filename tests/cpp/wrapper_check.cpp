@@ -73,6 +73,8 @@ int main(int argc, char** argv) {
   p.max_iters = 20;
   const rsfgpu::Volume phi = rsfgpu::evolve(phi0, img, p);
   dump(out + "/evolve_phi.raw", phi);
+  // two z-slabs with peer-linked halos (one device here): the same bits
+  dump(out + "/evolve_multi_phi.raw", rsfgpu::evolve_multi(phi0, img, p, {0, 0}));
   dump(out + "/mask.raw", rsfgpu::extract_mask(phi));
 
   const rsfgpu::TileLayout L = rsfgpu::plan_tiles(img.dims, {nx / 2, ny / 2, nz / 2}, p.sigma1, p.sigma2);

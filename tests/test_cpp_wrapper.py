@@ -65,6 +65,7 @@ def test_cpp_wrapper_gpu_matches_api(wrapper_bin, tmp_path, ref):
     p = rsf.RsfParams(sigma1=2.0, max_iters=20)
     phi = rsf.evolve(phi0, img, p)
     assert np.array_equal(load("evolve_phi.raw"), phi)
+    assert np.array_equal(load("evolve_multi_phi.raw"), phi)  # rsfgpu::evolve_multi, two linked slabs
     assert np.array_equal(load("mask.raw"), rsf.extract_mask(phi))
 
     phi_p, mask_p, warn = rsf.run_pipeline(img, p, (nx // 2, ny // 2, nz // 2))
