@@ -80,6 +80,12 @@ STRONG = {
 }
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 ALGO_BYTES = 12  # read phi, read I, write phi' (fp32, sigma2 = 0) per voxel-iteration
+# FP32 FMA-pipe lane-operations per voxel-iteration of the two kernels (FFMA/FMUL/FADD count 1,
+# the packed f32x2 forms 2), from ncu's per-opcode instruction counts at 512^3, sigma1 = 3
+# (profiles/r02_final_opcodes.txt), and the measured FMA-pipe peak of this B200 pool
+# (profiles/r01_fma_peak.txt: 36.87 T lane-ops/s, FFMA2 19-tap convolution microbenchmark).
+FP32_OPS = {"xy": 90.2, "zst": 93.0}
+FP32_PEAK_T = 36.87
 
 
 def peaks():
@@ -300,6 +306,16 @@ def bench_single(args):
                 "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
                 "kernel_share": {k: round(v / sum(kern.values()), 3) for k, v in kern.items()},
                 "step_frac": round(ALGO_BYTES * value / 1e9 / peak, 4)}
+    # The path is FP32-throughput-bound: the same kernels against the FMA pipe.
+    fp32_roofline = {"bound": "fp32 (FMA pipe; tensor cores unused)",
+                     "ops_per_voxel_iter": round(sum(FP32_OPS.values()), 1),
+                     "achieved": round(sum(FP32_OPS.values()) * value / 1e12, 2),
+                     "peak": FP32_PEAK_T, "unit": "T FMA-pipe lane-ops/s",
+                     "frac": round(sum(FP32_OPS.values()) * value / 1e12 / FP32_PEAK_T, 4),
+                     "kernel_frac": {k: round(FP32_OPS[k] * nvox / (kern[k] * 1e-3) / 1e12 / FP32_PEAK_T, 4)
+                                     for k in kern},
+                     "basis": "ncu per-opcode counts (profiles/r02_final_opcodes.txt) x voxel-iter/s; peak = "
+                              "measured FFMA2 throughput (profiles/r01_fma_peak.txt)"}
 
     # ---- 14-row stage profile (rsf::KernelProfile) over a few steps
     stage = rsf.KernelProfile()
@@ -371,7 +387,8 @@ def bench_single(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference phantom spec, seeded)",
-           "config": workload_config(1, args.fields), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "config": workload_config(1, args.fields), "roofline": roofline, "fp32_roofline": fp32_roofline,
+           "cpu_baseline": cpu, "e2e": e2e,
            "parity": parity, "stage_ms_per_iter": stage_rows, "gpu_launches": launches, "clocks": clk.summary()}
     print(json.dumps(out), flush=True)
 
