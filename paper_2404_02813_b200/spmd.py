@@ -9,10 +9,11 @@ monolithic volume, so any decomposition is bitwise identical to one GPU.
 
 * ``plan_slabs``   -- the partition (shared by every backend and the CPU tests).
 * ``SlabSet``      -- one process driving P slabs on one or more local GPUs;
-                      halos move with device/peer copies (rsfg_slab_exchange).
-* ``DistSlab``     -- one slab per rank; halos move with torch.distributed
-                      (NCCL send/recv over NVLink) on views of the slab's own
-                      device buffers, overlapped with the interior work.
+                      halos pushed over peer links (rsfg_slab_link, default)
+                      or exchanged between the step halves (rsfg_slab_exchange).
+* ``DistSlab``     -- one slab per rank; halos pushed over CUDA-IPC peer links
+                      (transport="ipc"), NCCL send/recv ("device") or
+                      host-staged gloo ("host").
 """
 from __future__ import annotations
 
@@ -145,13 +146,14 @@ class Slab:
 class SlabSet:
     """P slabs in one process (one or several local GPUs).
 
-    linked=False: halos move with rsfg_slab_exchange between the interior and
-    finish halves of every step.  linked=True: peer halo links
-    (rsfg_slab_link) -- each slab pushes its boundary planes into its
-    neighbours' halos after its step and bumps their flags; no host sync."""
+    linked=True (default): peer halo links (rsfg_slab_link) -- each slab
+    pushes its boundary planes into its neighbours' halos after its step and
+    bumps their flags; no host sync, the copies overlap the next step's
+    interior work.  linked=False: halos move with rsfg_slab_exchange between
+    the interior and finish halves of every step."""
 
     def __init__(self, phi0, I, p: RsfParams, parts: int, *, fields=2, devices=None, check_every=25,
-                 linked=False):
+                 linked=True):
         nz, ny, nx = phi0.shape
         self.nx, self.ny = nx, ny
         self.check_every = max(1, check_every)
@@ -240,9 +242,9 @@ class _DevView:
 
 
 class DistSlab:
-    """One slab per rank; halo exchange with torch.distributed (NCCL on GPUs).
+    """One slab per rank (torchrun, one process per GPU).
 
-    transport="ipc" is the B200-native data path: peer halo links over CUDA IPC
+    transport="ipc" (default) is the B200-native data path: peer halo links over CUDA IPC
     (rsfg_slab_link) -- each rank copies its boundary planes straight into its
     neighbours' halo rows over NVLink and bumps their flag words; the process
     group only carries the one-time descriptor exchange and the scalar
@@ -254,7 +256,7 @@ class DistSlab:
     lets several ranks share one GPU, which is how this path is tested on
     single-GPU machines (tests/test_gpu_distslab.py)."""
 
-    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None, transport="device",
+    def __init__(self, phi0, I, p: RsfParams, *, fields=2, rank=None, world=None, device=None, transport="ipc",
                  check_every=25):
         import torch
         self.check_every = max(1, check_every)

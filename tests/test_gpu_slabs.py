@@ -15,7 +15,7 @@ def test_slabs_bitwise(parts, fields):
     img, phi, _ = case(40, 36, 32)
     p = rsf.RsfParams(sigma1=3.0)
     st = rsf.init_evolution(phi, img, p, fields=fields)
-    ss = SlabSet(np.array(phi), np.array(img), p, parts, fields=fields)
+    ss = SlabSet(np.array(phi), np.array(img), p, parts, fields=fields, linked=False)  # exchange mode
     for _ in range(6):
         st.step()
         ss.step()
