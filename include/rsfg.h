@@ -260,12 +260,14 @@ int rsfg_slab_step_linked(rsfg_slab* s);
 
 /* rsf::evolve over n_devices GPUs of this process (the
  * north_star's rsfg_evolve(..., n_gpus, ...)): balanced z-slabs on
- * devices[0..n), linked halos (above), HOST buffers like rsfg_evolve.
- * Bitwise equal to rsfg_evolve on one device.  A device may repeat (several
- * slabs on one GPU).  Phase times in the report are host wall clock. */
+ * devices[0..n), linked halos (above), HOST buffers like rsfg_evolve, the
+ * same convergence stop and StopCheck callback (stop may be NULL; it gets
+ * the whole volume's phi, gathered from the slabs).  Bitwise equal to
+ * rsfg_evolve on one device.  A device may repeat (several slabs on one
+ * GPU).  Phase times in the report are host wall clock. */
 int rsfg_evolve_multi(const float* image, float* phi_inout, int32_t nx, int32_t ny, int32_t nz,
                       const rsfg_params* p, const rsfg_options* o, const int32_t* devices, int32_t n_devices,
-                      rsfg_report* report);
+                      rsfg_stop_fn stop, void* user, int32_t stop_every, rsfg_report* report);
 int rsfg_slab_download(rsfg_slab* s, float* phi_owned);
 int rsfg_slab_device_phi(rsfg_slab* s, float** d_phi_held);
 int64_t rsfg_slab_launches(const rsfg_slab* s);

@@ -189,17 +189,25 @@ inline Volume evolve(Volume phi0, const Volume& I, const RsfParams& p, StopCheck
 
 // rsf::evolve over several GPUs of this process (rsfg_evolve_multi): z-slabs
 // on `devices` with their halos pushed over NVLink peer memory every step;
-// bitwise equal to evolve() on one GPU.  (No StopCheck: it runs max_iters
-// steps or stops on convergence_fraction.)
+// bitwise equal to evolve() on one GPU; same StopCheck semantics.
 inline Volume evolve_multi(Volume phi0, const Volume& I, const RsfParams& p, const std::vector<int>& devices,
-                           const rsfg_options* options = nullptr) {
+                           StopCheck stop = nullptr, int stop_every = 25, const rsfg_options* options = nullptr) {
   p.validate();
   check_same_dims(phi0, I, "evolve");
   if (devices.empty()) throw param_error("evolve_multi: no devices");
   const rsfg_params cp = p.c();
   std::vector<int32_t> dv(devices.begin(), devices.end());
+  struct Ctx {
+    StopCheck* stop;
+  } ctx{&stop};
+  auto tramp = [](const float* phi, int32_t nx, int32_t ny, int32_t nz, int32_t it, void* u) -> int {
+    auto* c = static_cast<Ctx*>(u);
+    Volume v(nx, ny, nz);
+    std::memcpy(v.data.data(), phi, v.voxels() * sizeof(float));
+    return (*c->stop)(v, it) ? 1 : 0;
+  };
   check(rsfg_evolve_multi(I.data.data(), phi0.data.data(), I.dims.nx, I.dims.ny, I.dims.nz, &cp, options, dv.data(),
-                          (int32_t)dv.size(), nullptr));
+                          (int32_t)dv.size(), stop ? +tramp : nullptr, &ctx, stop_every, nullptr));
   return phi0;
 }
 

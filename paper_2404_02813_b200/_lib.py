@@ -139,8 +139,8 @@ SIGNATURES = {
     "rsfg_slab_peer_desc": (C.c_int, [VP, VP, I32]),
     "rsfg_slab_link": (C.c_int, [VP, I32, VP]),
     "rsfg_slab_step_linked": (C.c_int, [VP]),
-    "rsfg_evolve_multi": (C.c_int, [FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options), P(I32), I32,
-                                    P(rsfg_report)]),
+    "rsfg_evolve_multi": (C.c_int, [FP, FP, I32, I32, I32, P(rsfg_params), P(rsfg_options), P(I32), I32, STOP_FN,
+                                    VP, I32, P(rsfg_report)]),
     "rsfg_stage_name": (C.c_char_p, [I32]),
     "rsfg_stage_carrier": (C.c_int32, [I32]),
     "rsfg_state_step_profiled": (C.c_int, [VP, P(C.c_double), P(C.c_double)]),

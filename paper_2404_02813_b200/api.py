@@ -168,10 +168,12 @@ def evolve(phi0, I, p: RsfParams, stop=None, stop_every: int = 25, profile: Kern
     return phi[0] if squeeze else phi
 
 
-def evolve_multi(phi0, I, p: RsfParams, devices, *, fields: int = 2, report: L.rsfg_report | None = None):
+def evolve_multi(phi0, I, p: RsfParams, devices, stop=None, stop_every: int = 25, *, fields: int = 2,
+                 report: L.rsfg_report | None = None):
     """rsf::evolve over several GPUs of this process (rsfg_evolve_multi):
     z-slabs on ``devices`` (a device may repeat) with peer halo links;
-    bitwise equal to ``evolve`` on one device."""
+    bitwise equal to ``evolve`` on one device.  ``stop(phi, iteration)`` as in
+    ``evolve`` (phi gathered from the slabs)."""
     phi = _vol(phi0, "phi0").copy()
     img = _vol(I, "I")
     _check_same(phi, img, "evolve")
@@ -180,8 +182,13 @@ def evolve_multi(phi0, I, p: RsfParams, devices, *, fields: int = 2, report: L.r
     opt = options(fields, int(devices[0]))
     devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
     rep = report if report is not None else L.rsfg_report()
+    cb = L.STOP_FN(0)
+    if stop is not None:
+        def _cb(ptr, cx, cy, cz, it, _u):
+            return 1 if stop(np.ctypeslib.as_array(ptr, shape=(cz, cy, cx)).copy(), it) else 0
+        cb = L.STOP_FN(_cb)
     check(L.load().rsfg_evolve_multi(_ptr(img), _ptr(phi), nx, ny, nz, C.byref(cp), C.byref(opt), devs,
-                                     len(devices), C.byref(rep)))
+                                     len(devices), cb, None, stop_every, C.byref(rep)))
     return phi
 
 

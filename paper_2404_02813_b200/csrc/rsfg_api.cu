@@ -1621,6 +1621,7 @@ __attribute__((visibility("default"))) int rsfg_slab_step_linked(rsfg_slab* s) {
 __attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image, float* phi, int32_t nx, int32_t ny,
                                                              int32_t nz, const rsfg_params* p, const rsfg_options* o,
                                                              const int32_t* devices, int32_t n_devices,
+                                                             rsfg_stop_fn stop, void* user, int32_t stop_every,
                                                              rsfg_report* rep) {
   rsfg_report local{};
   if (!rep) rep = &local;
@@ -1632,7 +1633,7 @@ __attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image,
   if (o) opt = *o;
   if (n_devices == 1 || nz == 1) {
     opt.device = devices[0];
-    return rsfg_evolve(image, phi, nx, ny, nz, p, &opt, nullptr, nullptr, 0, rep);
+    return rsfg_evolve(image, phi, nx, ny, nz, p, &opt, stop, user, stop_every, rep);
   }
   rsfg::Taps t1, t2;
   if (int rc = make_taps(p->sigma1, t1)) return rc;
@@ -1693,11 +1694,13 @@ __attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image,
   long long l0 = 0;
   for (rsfg_slab* s : sl) l0 += s->launches;
   int pending = 0;
+  std::vector<float> host_phi;
   for (int it = 0; it < p->max_iters; ++it) {
     for (rsfg_slab* s : sl)
       if (int rc = step_linked(s)) return rc;
     ++pending;
-    if (per_step || pending == check_every || it + 1 == p->max_iters) {
+    const bool want_stop = stop && stop_every > 0 && (it + 1) % stop_every == 0;
+    if (per_step || want_stop || pending == check_every || it + 1 == p->max_iters) {
       long long sc_all = 0, best_idx = -1;
       int best_it = 0;
       for (rsfg_slab* s : sl) {
@@ -1720,6 +1723,15 @@ __attribute__((visibility("default"))) int rsfg_evolve_multi(const float* image,
         return fail(RSFG_ERR_BLOWUP, buf);
       }
       if (per_step && rep->last_sign_change_fraction < p->convergence_fraction) break;  // rsf.cpp:378
+      if (want_stop) {  // rsf.cpp:379-381: StopCheck with the whole volume's current phi
+        host_phi.resize((size_t)nx * ny * nz);
+        for (rsfg_slab* s : sl) {
+          CUDA_TRY(cudaSetDevice(s->dev));
+          CUDA_TRY(rsfg::copy_d2h(host_phi.data() + (size_t)s->z0 * plane, s->phi[s->cur] + s->off(s->z0),
+                                  s->owned() * sizeof(float), s->stream));
+        }
+        if (stop(host_phi.data(), nx, ny, nz, it + 1, user)) break;
+      }
     }
   }
   for (rsfg_slab* s : sl) CUDA_TRY(cudaStreamSynchronize(s->stream));

@@ -79,6 +79,16 @@ def test_evolve_multi_bitwise(n):
     got = rsf.evolve_multi(phi, img, p, [0] * n, report=rep)
     assert np.array_equal(got, rsf.evolve(phi, img, p))
     assert rep.iterations == 30 and rep.gpu_launches > 0
+    # StopCheck (rsf.cpp:379-381): called with the gathered volume every 10 steps, stop at 20
+    seen = []
+
+    def stop(phi_now, it):
+        seen.append((it, phi_now.shape))
+        return it >= 20
+
+    got_s = rsf.evolve_multi(phi, img, p, [0] * n, stop, 10)
+    assert seen == [(10, phi.shape), (20, phi.shape)]
+    assert np.array_equal(got_s, rsf.evolve(phi, img, rsf.RsfParams(sigma1=3.0, max_iters=20)))
 
 
 def test_evolve_multi_blowup_and_thin():
