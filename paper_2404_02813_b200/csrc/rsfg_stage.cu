@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -57,20 +58,77 @@ bool pool_ready(Pool& p) {
   return p.ok = true;
 }
 
+// Persistent memcpy workers (thread creation per chunk cost ~0.1 ms per 16 MB
+// chunk): the caller posts one job, every worker copies its slice, the
+// caller copies slice 0 and waits for the rest.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) : n_(n) {
+    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { run(t); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      quit_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void copy(void* dst, const void* src, size_t n) {
+    if (n_ == 1 || n < (1u << 20)) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      n_bytes_ = n;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    slice(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void slice(int t) {
+    const size_t per = (n_bytes_ + n_ - 1) / n_;
+    const size_t a = std::min(n_bytes_, t * per), b = std::min(n_bytes_, a + per);
+    if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+  }
+  void run(int t) {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (quit_) return;
+      }
+      slice(t);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  unsigned long long gen_ = 0;
+  bool quit_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t n_bytes_ = 0;
+  int pending_ = 0;
+};
+
 void par_memcpy(void* dst, const void* src, size_t n) {
-  const int nt = copy_threads();
-  const size_t per = (n + nt - 1) / nt;
-  if (n < (1u << 20) || nt == 1) {
-    std::memcpy(dst, src, n);
-    return;
-  }
-  std::thread th[kMaxThreads - 1];
-  for (int t = 1; t < nt; ++t) {
-    const size_t a = std::min(n, t * per), b = std::min(n, a + per);
-    th[t - 1] = std::thread([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
-  }
-  std::memcpy(dst, src, std::min(n, per));
-  for (int t = 1; t < nt; ++t) th[t - 1].join();
+  static CopyPool pool(copy_threads());  // used under Pool::mu (one copy at a time)
+  pool.copy(dst, src, n);
 }
 
 }  // namespace
