@@ -89,3 +89,51 @@ def test_slab_plan():
         plan_slabs(20, 4, 9)
     assert held_range(0, 64, 512, 9) == (0, 73)
     assert held_range(64, 128, 512, 9) == (55, 137)
+
+
+@pytest.fixture(scope="module")
+def c_caller(tmp_path_factory):
+    """tests/c/abi_check.c compiled as C99 against include/rsfg.h + librsfg.so."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    from paper_2404_02813_b200._lib import LIB_PATH
+    root = Path(__file__).resolve().parents[1]
+    out = tmp_path_factory.mktemp("c") / "abi_check"
+    lib = LIB_PATH.parent
+    subprocess.run(["gcc", "-std=c99", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{root / 'include'}",
+                    str(root / "tests" / "c" / "abi_check.c"), f"-L{lib}", "-lrsfg", f"-Wl,-rpath,{lib}", "-o",
+                    str(out)], check=True, capture_output=True, text=True)
+    return out
+
+
+def test_plain_c_caller_cpu(c_caller, oracle):
+    """A C99 host binds the boundary with no C++ or Python in between."""
+    import json
+    import subprocess
+    r = json.loads(subprocess.run([str(c_caller), "cpu"], check=True, capture_output=True, text=True).stdout)
+    assert r["default_ok"] == 1 and r["rc_dt"] == 1 and r["msg"] == "RsfParams: dt must be > 0"
+    assert r["radius"] == 9 and r["w9"] == oracle.gaussian_kernel(3.0)[9]
+    assert r["stage2"] == "K*H-I" and r["stage11"] == "R-combine" and r["version"].startswith("rsfg")
+    assert r["n_tiles"] > 0 and r["curtain"] == 6
+
+
+@pytest.mark.gpu
+def test_plain_c_caller_gpu(c_caller, tmp_path):
+    import json
+    import subprocess
+    import paper_2404_02813_b200 as rsf
+    from _inputs import case
+    nx, ny, nz = 64, 40, 36
+    img, phi, _ = case(nx, ny, nz, n_branches=3)
+    (tmp_path / "img.raw").write_bytes(np.ascontiguousarray(img, np.float32).tobytes())
+    (tmp_path / "phi.raw").write_bytes(np.ascontiguousarray(phi, np.float32).tobytes())
+    r = json.loads(subprocess.run([str(c_caller), "gpu", str(nx), str(ny), str(nz), str(tmp_path / "img.raw"),
+                                   str(tmp_path / "phi.raw"), str(tmp_path)], check=True, capture_output=True,
+                                  text=True).stdout)
+    assert r["iterations"] == 12 and r["launches"] > 0
+    want = rsf.evolve(phi, img, rsf.RsfParams(sigma1=3.0, max_iters=12))
+    got = np.fromfile(tmp_path / "c_evolve.raw", np.float32).reshape(nz, ny, nx)
+    got_m = np.fromfile(tmp_path / "c_evolve_multi.raw", np.float32).reshape(nz, ny, nx)
+    assert np.array_equal(got, want) and np.array_equal(got_m, want)
