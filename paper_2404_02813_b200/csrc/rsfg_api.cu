@@ -411,7 +411,8 @@ void make_xy2_maps(rsfg_slab* s) {
   // extra work cancels the gain, profiles/r01_hh_mode.txt).  RSFG_HH=0|1
   // overrides.  Needs zst4 (it writes the pairs).
   const char* hh_env = std::getenv("RSFG_HH");
-  const bool hh_want = hh_env ? hh_env[0] == '1' : s->t1.r <= 9;
+  // (the stored-Heaviside kernels exist for R <= 9 only: RSFG_HH=1 cannot force it past that)
+  const bool hh_want = (hh_env ? hh_env[0] == '1' : true) && s->t1.r <= 9;
   if (hh_want && s->xy2_ty == 32 && s->fields == 2 && s->t2.r == 0 && s->zmaps[0].valid && s->hh) {
     CUtensorMap m;
     if (encode_map(&m, s->hh, 2 * s->nx, s->ny, planes, 2 * bx, by, 1)) {

@@ -45,8 +45,11 @@ def main():
         ms = e0.elapsed_time(e1) / a.steps
         fl = C.c_int32()
         check(lib.rsfg_state_variant(h, C.byref(fl), None, None))
+        prof = (C.c_double * 2)()
+        check(lib.rsfg_state_profile(h, 5, prof))
         r = (len(rsf.gaussian_kernel(s)) - 1) // 2
         print(json.dumps({"sigma1": s, "radius": r, "variant_flags": fl.value, "ms_per_step": round(ms, 3),
+                          "kernel_ms": {"xy": round(prof[0], 3), "zst": round(prof[1], 3)},
                           "voxel_iter_per_s": n ** 3 / (ms * 1e-3)}), flush=True)
         lib.rsfg_state_destroy(h)
 
