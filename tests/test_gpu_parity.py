@@ -178,7 +178,7 @@ def test_stored_heaviside_bitwise(rsf, shape, monkeypatch):
     assert np.array_equal(st.phi, st2.phi)
 
 
-@pytest.mark.parametrize("sigma1", [7.0, 2.5])  # R=21 (generic path), R=8
+@pytest.mark.parametrize("sigma1", [9.0, 7.0, 2.5])  # R=27 (generic runtime-tap path), R=21, R=8
 def test_generic_and_other_radii(rsf, oracle, sigma1):
     from _oracle import params
     img, phi, _ = case(48, 40, 44)

@@ -42,8 +42,8 @@ def test_slabs_bitwise_interior_tiles(parts):
 def test_slab_generic_radius_bitwise():
     import paper_2404_02813_b200 as rsf
     from paper_2404_02813_b200.spmd import SlabSet
-    img, phi, _ = case(40, 36, 48)
-    p = rsf.RsfParams(sigma1=7.0)  # R = 21: generic path
+    img, phi, _ = case(40, 36, 60)
+    p = rsf.RsfParams(sigma1=9.0)  # R = 27: generic runtime-tap path (specialised kernels stop at R = 24)
     st = rsf.init_evolution(phi, img, p)
     ss = SlabSet(np.array(phi), np.array(img), p, 2)
     for _ in range(3):
@@ -52,7 +52,7 @@ def test_slab_generic_radius_bitwise():
     assert np.array_equal(ss.phi(), st.phi)
 
 
-@pytest.mark.parametrize("parts,fields,sigma1", [(2, 2, 3.0), (3, 4, 3.0), (4, 2, 2.0), (2, 2, 7.0)])
+@pytest.mark.parametrize("parts,fields,sigma1", [(2, 2, 3.0), (3, 4, 3.0), (4, 2, 2.0), (2, 2, 7.0), (2, 2, 9.0)])
 def test_linked_slabs_bitwise(parts, fields, sigma1):
     """Peer halo links (rsfg_slab_link / step_linked): pushes of the boundary
     planes + flag waits, no host synchronisation, several slabs on one GPU."""

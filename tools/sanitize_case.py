@@ -27,7 +27,8 @@ def case(nx, ny, nz, seed=0):
 
 def main():
     runs = [((72, 40, 36), 3.0, 2), ((72, 40, 36), 3.0, 4), ((70, 34, 30), 3.0, 2),  # LDG fallback (nx % 4)
-            ((96, 72, 40), 6.0, 2), ((64, 48, 40), 7.0, 2), ((68, 44, 42), 1.0, 2)]
+            ((96, 72, 40), 6.0, 2), ((64, 48, 40), 7.0, 2), ((64, 48, 60), 9.0, 2),  # R 21 specialised, R 27 generic
+            ((68, 44, 42), 1.0, 2)]
     for shape, s1, fields in runs:
         img, phi = case(*shape)
         out = rsf.evolve(phi, img, rsf.RsfParams(sigma1=s1, max_iters=3), fields=fields)
