@@ -407,12 +407,12 @@ void make_xy2_maps(rsfg_slab* s) {
   s->xy2maps[0].valid = s->xy2maps[1].valid = true;
   // Stored-Heaviside mode: kernel 2 evaluates H once per voxel instead of
   // kernel 1 on every haloed tile.  It pays while the Heaviside is a large
-  // share of kernel 1 (R <= 9: step -7 % at sigma 3; at R = 12 kernel 2's
-  // extra work cancels the gain, profiles/r01_hh_mode.txt).  RSFG_HH=0|1
-  // overrides.  Needs zst4 (it writes the pairs).
+  // share of kernel 1 and kernel 1's pair tiles fit two CTAs per SM: R <= 10
+  // (kHHMaxR; sigma 3: step -7 %, sigma 3.2: -7 %).  RSFG_HH=0 turns it off.
+  // Needs zst4 (it writes the pairs).
   const char* hh_env = std::getenv("RSFG_HH");
-  // (the stored-Heaviside kernels exist for R <= 9 only: RSFG_HH=1 cannot force it past that)
-  const bool hh_want = (hh_env ? hh_env[0] == '1' : true) && s->t1.r <= 9;
+  // (the stored-Heaviside kernels exist up to kHHMaxR: RSFG_HH=1 cannot force it past that)
+  const bool hh_want = (hh_env ? hh_env[0] == '1' : true) && s->t1.r <= rsfg::kHHMaxR;
   if (hh_want && s->xy2_ty == 32 && s->fields == 2 && s->t2.r == 0 && s->zmaps[0].valid && s->hh) {
     CUtensorMap m;
     if (encode_map(&m, s->hh, 2 * s->nx, s->ny, planes, 2 * bx, by, 1)) {

@@ -503,9 +503,9 @@ int xy2_hh_launch(const Geom& g, const Taps& t, float2* P0, int z_begin, int z_e
 template <int R, int NP, int TY>
 int xy2_launch(const Geom& g, const Taps& t, float inv_eps, float2* P0, float2* P1, int z_begin, int z_end,
                const XYMaps& m, cudaStream_t st) {
-  // the stored-Heaviside variant exists where the mode is used (R <= 9,
+  // the stored-Heaviside variant exists where the mode is used (R <= kHHMaxR,
   // 64 x 32 tiles; rsfg_api.cu make_xy2_maps)
-  if constexpr (NP == 1 && R <= 9 && TY == 32) {
+  if constexpr (NP == 1 && R <= kHHMaxR && TY == 32) {
     if (m.use_hh) return xy2_hh_launch<R, TY>(g, t, P0, z_begin, z_end, m, st);
   }
   if (m.use_hh && NP == 1) return -1;

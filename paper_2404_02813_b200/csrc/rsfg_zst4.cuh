@@ -457,11 +457,11 @@ int zst4_launch_v(const Geom& g, const Taps& t, const StepConsts& c, const StepB
 }
 
 // The stored-Heaviside variant exists for the radii where the mode pays
-// (R <= 9, rsfg_api.cu make_xy2_maps); elsewhere b.hh is never set.
+// (R <= kHHMaxR, rsfg_api.cu make_xy2_maps); elsewhere b.hh is never set.
 template <int R, int NP>
 int zst4_launch(const Geom& g, const Taps& t, const StepConsts& c, const StepBuffers& b, int z_begin, int z_end,
                 const ZMaps& m, cudaStream_t st) {
-  if constexpr (NP == 1 && R <= 9) {
+  if constexpr (NP == 1 && R <= kHHMaxR) {
     if (b.hh) return zst4_launch_v<R, NP, true>(g, t, c, b, z_begin, z_end, m, st);
   }
   if (b.hh) return -1;

@@ -155,12 +155,13 @@ def test_kernel2_variants_P2(rsf, oracle, zst4, monkeypatch):
     assert _rel_err(st.phi, ref) <= P2_TOL
 
 
+@pytest.mark.parametrize("sigma1", [3.0, 3.2])  # R = 9, R = 10 (the mode's largest radius)
 @pytest.mark.parametrize("shape", [(96, 28, 80), (40, 36, 32)])
-def test_stored_heaviside_bitwise(rsf, shape, monkeypatch):
+def test_stored_heaviside_bitwise(rsf, shape, sigma1, monkeypatch):
     """Kernel 2 writing (H-, H- I) for kernel 1 (default for fields=2,
-    sigma2=0) reproduces kernel 1's own Heaviside bit for bit (RSFG_HH=0)."""
+    sigma2=0, R <= 10) reproduces kernel 1's own Heaviside bit for bit (RSFG_HH=0)."""
     img, phi, _ = case(*shape)
-    p = _params(rsf, sigma1=3.0, max_iters=6)
+    p = _params(rsf, sigma1=sigma1, max_iters=6)
     monkeypatch.setenv("RSFG_HH", "1")
     a = rsf.evolve(phi, img, p)
     monkeypatch.setenv("RSFG_HH", "0")
@@ -178,7 +179,7 @@ def test_stored_heaviside_bitwise(rsf, shape, monkeypatch):
     assert np.array_equal(st.phi, st2.phi)
 
 
-@pytest.mark.parametrize("sigma1", [9.0, 7.0, 2.5])  # R=27 (generic runtime-tap path), R=21, R=8
+@pytest.mark.parametrize("sigma1", [9.0, 7.0, 3.2, 2.5])  # R=27 (generic runtime-tap path), R=21, R=10, R=8
 def test_generic_and_other_radii(rsf, oracle, sigma1):
     from _oracle import params
     img, phi, _ = case(48, 40, 44)
