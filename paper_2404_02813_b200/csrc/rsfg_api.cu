@@ -407,9 +407,9 @@ void make_xy2_maps(rsfg_slab* s) {
   s->xy2maps[0].valid = s->xy2maps[1].valid = true;
   // Stored-Heaviside mode: kernel 2 evaluates H once per voxel instead of
   // kernel 1 on every haloed tile.  It pays while the Heaviside is a large
-  // share of kernel 1 and kernel 1's pair tiles fit two CTAs per SM: R <= 10
-  // (kHHMaxR; sigma 3: step -7 %, sigma 3.2: -7 %).  RSFG_HH=0 turns it off.
-  // Needs zst4 (it writes the pairs).
+  // share of kernel 1 and kernel 1 keeps two CTAs per SM: R <= 12 (kHHMaxR;
+  // sigma 3: step -7 %, 3.2: -7 %, 4: -2 %; its pair tile is single-buffered
+  // past R = 10).  RSFG_HH=0 turns it off.  Needs zst4 (it writes the pairs).
   const char* hh_env = std::getenv("RSFG_HH");
   // (the stored-Heaviside kernels exist up to kHHMaxR: RSFG_HH=1 cannot force it past that)
   const bool hh_want = (hh_env ? hh_env[0] == '1' : true) && s->t1.r <= rsfg::kHHMaxR;

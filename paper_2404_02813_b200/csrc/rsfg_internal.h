@@ -59,10 +59,10 @@ enum StepMode { kUpdate = 0, kEnergy = 1 };
 // True when a fused, radius-specialised kernel exists for r.
 bool has_fast_radius(int r);
 // Largest radius with stored-Heaviside kernels (xy2_hh, zst4<.., HH>) and the
-// mode's default range: up to R = 10 kernel 1's two (H-, H- I) tile buffers
-// still fit two CTAs per SM; at R = 11-12 they do not and the mode measured
-// slower (sigma 3.5: 1.87 vs 1.73 ms/step; sigma 3.2, R = 10: 1.54 vs 1.66).
-constexpr int kHHMaxR = 10;
+// mode's default range.  Up to R = 10 kernel 1 double-buffers its (H-, H- I)
+// tile; at R = 11-12 it single-buffers it to keep two CTAs per SM (sigma 4:
+// 1.77 vs 1.80 ms/step without the mode; double-buffered it was 1.91).
+constexpr int kHHMaxR = 12;
 // Whether kernel 1's specialised variants fit shared memory for (r, fields):
 // xy2 with tile height ty (TMA, nx % 4 == 0) and the LDG-staged xy.
 bool xy2_fits(int r, int fields, int ty);

@@ -56,7 +56,12 @@ struct XY2 {
   static constexpr size_t kSmem = kHsBytes + kYsBytes + (kOsAlias ? 0 : kOsBytes) + 2 * kTile + 16;
   // stored-Heaviside variant (xy2_cta_hh): two (H-, H- I) tile buffers, Ys, Os
   static constexpr size_t kTileHH = ((size_t)BOXX * WY * sizeof(float2) + 127) & ~(size_t)127;
-  static constexpr size_t kSmemHH = 2 * kTileHH + kYsBytes + kOsBytes + 16;
+  // Two (H-, H- I) tile buffers (plane z+1 lands while plane z is filtered)
+  // while that still leaves two CTAs per SM; past that (R >= 11 at 64 x 32)
+  // one buffer, refilled as soon as the y pass has consumed it.
+  static constexpr bool kHHDouble = 2 * kTileHH + kYsBytes + kOsBytes + 16 <= 113 * 1024;
+  static constexpr int kHHBufs = kHHDouble ? 2 : 1;
+  static constexpr size_t kSmemHH = kHHBufs * kTileHH + kYsBytes + kOsBytes + 16;
   static constexpr int RG = NT / NPR;                     // row groups of phase A
   static constexpr int RITER = (WY + RG - 1) / RG;        // rows per phase-A thread
   static constexpr int YIT = (NP * WX * (TY / BY) + NT - 1) / NT;  // y-pass items per thread
@@ -323,8 +328,8 @@ __device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, floa
                                            int z_last, int x0, int y0, const CUtensorMap* map_hh,
                                            unsigned char* smem) {
   using C = XY2<R, 1, TY>;
-  float2* __restrict__ Ys = reinterpret_cast<float2*>(smem + 2 * C::kTileHH);                 // [TY][PY]
-  float2* __restrict__ Os = reinterpret_cast<float2*>(smem + 2 * C::kTileHH + C::kYsBytes);  // [TY][PO]
+  float2* __restrict__ Ys = reinterpret_cast<float2*>(smem + C::kHHBufs * C::kTileHH);                 // [TY][PY]
+  float2* __restrict__ Os = reinterpret_cast<float2*>(smem + C::kHHBufs * C::kTileHH + C::kYsBytes);  // [TY][PO]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kSmemHH - 16);
   const int tid = threadIdx.x;
   const int bx0 = x0 - R - C::SHIFT, by0 = y0 - R;
@@ -376,10 +381,10 @@ __device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, floa
 
 #pragma unroll 1
   for (int z = z_first; z < z_last; ++z) {
-    const int xb = (z - z_first) & 1;
+    const int xb = C::kHHDouble ? (z - z_first) & 1 : 0;
     float2* T = reinterpret_cast<float2*>(smem + xb * C::kTileHH);  // [WY][BOXX] (H-, H- I)
-    mbar_wait(bars + xb, (uint32_t)(((z - z_first) >> 1) & 1));
-    if (tid == 0 && z + 1 < z_last) {
+    mbar_wait(bars + xb, (uint32_t)((C::kHHDouble ? (z - z_first) >> 1 : z - z_first) & 1));
+    if (C::kHHDouble && tid == 0 && z + 1 < z_last) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(z + 1, xb ^ 1);
     }
@@ -422,6 +427,10 @@ __device__ __forceinline__ void xy2_cta_hh(const Geom& g, const Taps& taps, floa
       }
     }
     __syncthreads();
+    if (!C::kHHDouble && tid == 0 && z + 1 < z_last) {  // one buffer: the y pass has consumed it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(z + 1, 0);
+    }
     // ---- x pass (lanes walk rows of the odd-pitched Ys) into the staging tile
 #pragma unroll
     for (int i = 0; i < C::XIT; ++i) {
