@@ -393,8 +393,13 @@ void make_xy2_maps(rsfg_slab* s) {
   // shared memory); 64 x 32 (2 CTAs/SM) wins up to R = 12
   // (profiles/r01_xy2_tile_height.txt).  RSFG_XY2_TY=32|64 overrides.
   const char* ty = std::getenv("RSFG_XY2_TY");
-  // (R >= 19: the 64 x 64 tile's haloed pairs exceed shared memory; 64 x 32)
-  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32) : (s->t1.r >= 15 && s->t1.r <= 18 && s->fields == 2 ? 64 : 32);
+  // (R >= 19: the 64 x 64 tile's haloed pairs exceed shared memory; 64 x 32.
+  // The stored-Heaviside kernel 1 is a 64 x 32 tile at every radius.)
+  const char* hh_env0 = std::getenv("RSFG_HH");
+  const bool hh_possible = (hh_env0 ? hh_env0[0] == '1' : true) && s->t1.r <= rsfg::kHHMaxR && s->fields == 2 &&
+                           s->t2.r == 0;
+  s->xy2_ty = ty ? (std::atoi(ty) == 64 ? 64 : 32)
+                 : (!hh_possible && s->t1.r >= 15 && s->t1.r <= 18 && s->fields == 2 ? 64 : 32);
   int bx = 0, by = 0;
   if (!rsfg::xy2_box(s->t1.r, s->xy2_ty, &bx, &by)) return;
   const int planes = s->ze - s->zb;
@@ -405,11 +410,10 @@ void make_xy2_maps(rsfg_slab* s) {
     s->xy2maps[b].img = img;
   }
   s->xy2maps[0].valid = s->xy2maps[1].valid = true;
-  // Stored-Heaviside mode: kernel 2 evaluates H once per voxel instead of
-  // kernel 1 on every haloed tile.  It pays while the Heaviside is a large
-  // share of kernel 1 and kernel 1 keeps two CTAs per SM: R <= 12 (kHHMaxR;
-  // sigma 3: step -7 %, 3.2: -7 %, 4: -2 %; its pair tile is single-buffered
-  // past R = 10).  RSFG_HH=0 turns it off.  Needs zst4 (it writes the pairs).
+  // Stored-Heaviside mode (fields = 2, sigma2 = 0, every specialised radius):
+  // kernel 2 evaluates H once per voxel instead of kernel 1 on every haloed
+  // tile (rsfg_internal.h kHHMaxR).  RSFG_HH=0 turns it off.  Needs zst4 (it
+  // writes the pairs).
   const char* hh_env = std::getenv("RSFG_HH");
   // (the stored-Heaviside kernels exist up to kHHMaxR: RSFG_HH=1 cannot force it past that)
   const bool hh_want = (hh_env ? hh_env[0] == '1' : true) && s->t1.r <= rsfg::kHHMaxR;

@@ -58,11 +58,14 @@ enum StepMode { kUpdate = 0, kEnergy = 1 };
 
 // True when a fused, radius-specialised kernel exists for r.
 bool has_fast_radius(int r);
-// Largest radius with stored-Heaviside kernels (xy2_hh, zst4<.., HH>) and the
-// mode's default range.  Up to R = 10 kernel 1 double-buffers its (H-, H- I)
-// tile; at R = 11-12 it single-buffers it to keep two CTAs per SM (sigma 4:
-// 1.77 vs 1.80 ms/step without the mode; double-buffered it was 1.91).
-constexpr int kHHMaxR = 12;
+// Largest radius with stored-Heaviside kernels (xy2_hh, zst4<.., HH>): every
+// specialised radius.  The mode is the default for fields = 2, sigma2 = 0:
+// kernel 2 evaluates H once per voxel, kernel 1 skips the Heaviside on its
+// (64 + 2R) x (32 + 2R) halo tile.  Up to R = 10 kernel 1 double-buffers the
+// pair tile, past that it single-buffers it (two CTAs per SM up to R = 18).
+// Measured step gains: sigma 3 -7 %, 4 -2 %, 5 -8 %, 6 -8 %, 7 -22 %, 8 -11 %
+// (profiles/r02_hh_mode_ab.jsonl).
+constexpr int kHHMaxR = 24;
 // Whether kernel 1's specialised variants fit shared memory for (r, fields):
 // xy2 with tile height ty (TMA, nx % 4 == 0) and the LDG-staged xy.
 bool xy2_fits(int r, int fields, int ty);

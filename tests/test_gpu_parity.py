@@ -155,11 +155,11 @@ def test_kernel2_variants_P2(rsf, oracle, zst4, monkeypatch):
     assert _rel_err(st.phi, ref) <= P2_TOL
 
 
-@pytest.mark.parametrize("sigma1", [3.0, 3.2, 4.0])  # R = 9, 10 (double-buffered pair tile), 12 (single)
+@pytest.mark.parametrize("sigma1", [3.0, 3.2, 4.0, 6.0, 7.0])  # R 9, 10 (double-buffered pair tile), 12, 18, 21
 @pytest.mark.parametrize("shape", [(96, 28, 80), (40, 36, 32)])
 def test_stored_heaviside_bitwise(rsf, shape, sigma1, monkeypatch):
     """Kernel 2 writing (H-, H- I) for kernel 1 (default for fields=2,
-    sigma2=0, R <= 12) reproduces kernel 1's own Heaviside bit for bit (RSFG_HH=0)."""
+    sigma2=0) reproduces kernel 1's own Heaviside bit for bit (RSFG_HH=0)."""
     img, phi, _ = case(*shape)
     p = _params(rsf, sigma1=sigma1, max_iters=6)
     monkeypatch.setenv("RSFG_HH", "1")
