@@ -39,12 +39,28 @@ namespace {
 // halo = 3 full warps) measured slower than 32 x 8 (zst 1.044 vs 0.962 ms)
 constexpr int kZ4TallTY = RSFG_Z4_TALL_TY;
 
+// Shared memory of a 32 x ty zst4 CTA at radius r (the Z4 layout below).
+constexpr size_t z4_smem(int r, int np, int ty) {
+  return (size_t)np * (8 + 2 * r) * 32 * ty * 8 + (size_t)8 * ((40 * (ty + 4) + 31) & ~31) * 4 +
+         (size_t)8 * (np == 1 ? 2 : 1) * 32 * ty * 4 + (size_t)2 * 2 * 34 * (ty + 2) * 4 + 128;
+}
+// Column-tile height.  fields = 2: 32 x 8, or 32 x 6 where the 8-row z-pass
+// window (8 + 2R planes of P) would leave one CTA per SM (R >= 16), or 32 x 4.
+// fields = 4: 32 x 8, 32 x 4 from R = 17.
+constexpr int z4_ty(int r, int np) {
+  if (np == 2) return r >= 17 ? 4 : 8;
+  if (r <= 9) return kZ4TallTY;
+  if (z4_smem(r, np, 8) + 1024 <= 114 * 1024) return 8;
+  if (z4_smem(r, np, 6) + 1024 <= 114 * 1024) return 6;
+  return 4;
+}
+
 template <int R, int NP>
 struct Z4 {
-  // 32 x 8 columns; 32 x 4 for large radii, whose z-pass window (8 + 2R
-  // planes of P) would otherwise leave one CTA per SM.
-  static constexpr int TX = 32, TY = R >= 17 ? 4 : (R <= 9 && NP == 1 ? kZ4TallTY : 8), NT = TX * TY;
-  static constexpr int BX = 40, BY = TY + 4, SLOT = BX * BY;  // phi TMA box (floats): x0-4.., y0-2..
+  static constexpr int TX = 32, TY = z4_ty(R, NP), NT = TX * TY;
+  // phi TMA box (floats): x0-4.., y0-2..; ring slots padded to 128 bytes
+  // (cp.async.bulk.tensor destinations must be 128-byte aligned)
+  static constexpr int BX = 40, BY = TY + 4, BOXF = BX * BY, SLOT = (BOXF + 31) & ~31;
   static constexpr int NXr = TX + 2, NYr = TY + 2, NPL = NXr * NYr;  // normal plane, halo 1
   static constexpr int kHalo = 2 * TX + 2 * TY;           // halo positions kappa reads (no corners)
   static constexpr int kProducer = 3 * 32;                // TMA-issuing thread (warp 3, no halo work)
@@ -60,10 +76,10 @@ struct Z4 {
   static constexpr size_t kNrBytes = (size_t)2 * 2 * NPL * sizeof(float);
   static constexpr size_t kSmem = kPBytes + kPhiBytes + kKBytes + kNrBytes + 16 * sizeof(uint64_t);
   // CTAs per SM the register budget is sized for: three 32 x 4 CTAs where their
-  // shared memory allows it (R 17-18), else two (one for 32 x 16 tiles)
+  // shared memory allows it, else two (one for 32 x 16 tiles)
   static constexpr int kMinBlocks =
       TY == 16 ? 1 : (TY == 4 && NP == 1 && 3 * (kSmem + 1024) <= 228 * 1024 ? 3 : 2);
-  static constexpr uint32_t kSlotTx = (uint32_t)((SLOT + NK * NT) * sizeof(float));
+  static constexpr uint32_t kSlotTx = (uint32_t)((BOXF + NK * NT) * sizeof(float));
 };
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
