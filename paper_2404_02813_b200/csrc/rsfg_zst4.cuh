@@ -77,8 +77,7 @@ struct Z4 {
   static constexpr size_t kSmem = kPBytes + kPhiBytes + kKBytes + kNrBytes + 16 * sizeof(uint64_t);
   // CTAs per SM the register budget is sized for: three 32 x 4 CTAs where their
   // shared memory allows it, else two (one for 32 x 16 tiles)
-  static constexpr int kMinBlocks =
-      TY == 16 ? 1 : (TY == 4 && NP == 1 && 3 * (kSmem + 1024) <= 228 * 1024 ? 3 : 2);
+  static constexpr int kMinBlocks = TY == 16 ? 1 : (NP == 1 && 3 * (kSmem + 1024) <= 228 * 1024 ? 3 : 2);
   static constexpr uint32_t kSlotTx = (uint32_t)((BOXF + NK * NT) * sizeof(float));
 };
 
