@@ -26,6 +26,16 @@ def case(nx, ny, nz, seed=0):
 
 
 def main():
+    if "--quick" in sys.argv:  # the pytest gate: stored-Heaviside xy2/zst4 (+ a face tile) and linked slabs
+        img, phi = case(72, 40, 36)
+        assert np.isfinite(rsf.evolve(phi, img, rsf.RsfParams(sigma1=3.0, max_iters=2))).all()
+        img, phi = case(96, 28, 48)
+        ss = SlabSet(phi, img, rsf.RsfParams(sigma1=2.0), 2, linked=True)
+        ss.step()
+        ss.step()
+        ss.close()
+        print("ok quick", flush=True)
+        return
     runs = [((72, 40, 36), 3.0, 2), ((72, 40, 36), 3.0, 4), ((70, 34, 30), 3.0, 2),  # LDG fallback (nx % 4)
             ((96, 72, 40), 6.0, 2), ((64, 48, 40), 7.0, 2), ((64, 48, 60), 9.0, 2),  # R 21 specialised, R 27 generic
             ((68, 44, 42), 1.0, 2)]
