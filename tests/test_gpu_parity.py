@@ -179,7 +179,8 @@ def test_stored_heaviside_bitwise(rsf, shape, sigma1, monkeypatch):
     assert np.array_equal(st.phi, st2.phi)
 
 
-@pytest.mark.parametrize("sigma1", [9.0, 7.0, 3.2, 2.5])  # R=27 (generic runtime-tap path), R=21, R=10, R=8
+# R = 27 (generic runtime-tap path), 24 (32x4 kernel-2 tiles), 21, 16 (first 32x6 tiles), 10, 8
+@pytest.mark.parametrize("sigma1", [9.0, 8.0, 7.0, 5.3, 3.2, 2.5])
 def test_generic_and_other_radii(rsf, oracle, sigma1):
     from _oracle import params
     img, phi, _ = case(48, 40, 44)
